@@ -1,0 +1,118 @@
+/*
+ * hexgram_b200.h -- C ABI of the B200 (sm_100a) Gram-integration library
+ * libhexgram_b200.so.
+ *
+ * This is the drop-in seam for the reference's compiled kernels.  In the
+ * reference (/root/reference/pkg/src/hexgram) control enters compiled code
+ * at the numba dispatchers selected in gram.py:
+ *
+ *   gram.py:127-136  _TENS_KERNELS[(space, loop_order)] ->
+ *                    tens_{l2,h1,hdiv,hcurl}_{std,alt}(p1,p2,p3,nodes,wts,kind,par,wgrid)
+ *                    (_kernels.py:356-1150), called at gram.py:154-157
+ *   gram.py:183-191  simp_{l2,h1,hdiv,hcurl}_const(p1,p2,p3,fall,kind,par,wmass)
+ *                    (_kernels.py:1169-1404)
+ *
+ * Each reference call integrates ONE element and returns a dense N x N
+ * matrix plus operation counters.  The entry points below integrate a BATCH
+ * of E independent elements per call (the reference's calls are pure and
+ * independent), writing packed upper triangles.
+ *
+ * Conventions
+ *   space  : 0 = H1, 1 = H(curl), 2 = H(div), 3 = L2   (spaces.py:30 order differs;
+ *            the codes here are the library's own)
+ *   path   : 0 = general map, sum factorization O(p^7)  (gram_tensorized)
+ *            1 = constant-Jacobian map, O(p^6)           (gram_simplified, kinds 0..2)
+ *   kind   : element-map kind codes of geometry.py:46-52
+ *            (0 identity, 1 diagonal-affine, 2 general-affine, 3 extrusion, 4 trilinear)
+ *   params : 24 doubles per element, layout of geometry.py:83-119
+ *   coef   : per-element scalar weight of the mass (zeroth-order) term only
+ *            (gram.py:66-98, _kernels.py:15-18); may be NULL (= 1)
+ *   wgrid  : optional per-element, per-quadrature-node mass weight
+ *            [E][L][L][L] (gram.py:78-90 sampled on the host); general path only;
+ *            overrides coef when non-NULL
+ *   out    : [E][N(N+1)/2] fp64, row-major packed upper triangle
+ *            (entry (r,c), r <= c, at r*N - r*(r-1)/2 + (c-r))
+ *   status : [E] int bit mask, written by the call: 0 ok; bit 0: det J <= 0 at
+ *            an evaluated point (the reference raises DegenerateMapError,
+ *            errors.py:12-20); bit 1: constant-Jacobian path asked for a map
+ *            kind > 2 (SimplificationNotApplicableError, gram.py:170-174)
+ *
+ * All pointers of hxg_gram_batched are DEVICE pointers; the call is
+ * stream-ordered, does no host synchronisation and is safe to issue from
+ * several host threads on distinct streams.  `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  Return values are HXG_OK or a negative
+ * HXG_ERR_* code; the Python layer maps them onto the reference's exception
+ * types (errors.py).
+ */
+#ifndef HEXGRAM_B200_H
+#define HEXGRAM_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    HXG_OK = 0,
+    HXG_ERR_ORDER = -1,        /* InvalidOrderError: p_d < 1, p_d > HXG_MAX_ORDER, bad L */
+    HXG_ERR_SPACE = -2,        /* unknown space / path code                                */
+    HXG_ERR_KIND = -3,         /* SimplificationNotApplicableError (gram.py:171-174)       */
+    HXG_ERR_WORKSPACE = -4,    /* workspace too small                                      */
+    HXG_ERR_CUDA = -5,         /* CUDA launch / runtime error                              */
+    HXG_ERR_ARG = -6           /* NULL pointer or negative count                           */
+};
+
+#define HXG_MAX_ORDER 12   /* poly1d.py:37 DEFAULT_P_MAX, cli.py:55 MAX_SUPPORTED_ORDER */
+#define HXG_MAX_RULE 16    /* 1D Gauss points supported by the device kernels           */
+
+/* library version, e.g. 100 for 0.1.0 */
+int hxg_version(void);
+const char *hxg_error_string(int code);
+
+/* spaces.py:67-80 -- number of basis functions N; <0 on bad arguments */
+int hxg_dim(int space, int p1, int p2, int p3);
+
+/* OpCounters.accumulations of the reference for the same call
+ * (closed forms; gram.py:45-50) */
+long long hxg_accumulations(int space, int path, int p1, int p2, int p3, int L);
+
+/* Size in doubles of the device 1D-table block used by hxg_gram_batched. */
+size_t hxg_tables_doubles(void);
+
+/* Build the 1D tables on the device (quadrature.py:47-66, _kernels.py:29-53,
+ * poly1d.py:140-266): Gauss-Legendre nodes/weights on (0,1) for L points,
+ * chi_k / chi'_k at the nodes, and the closed-form F tables.  If `nodes` and
+ * `weights` (device pointers, L each) are non-NULL they are used instead of
+ * the Gauss rule (a user-supplied Rule1D, gram.py:139-151). */
+int hxg_make_tables(int L, const double *nodes, const double *weights, double *tables,
+                    void *stream);
+
+/* Device workspace (bytes) needed by hxg_gram_batched for this call. */
+size_t hxg_workspace_size(int space, int path, int p1, int p2, int p3, int L, int E);
+
+/* Batched Gram integration -- replaces tens_*_{std,alt} (path 0) and
+ * simp_*_const (path 1).  tables from hxg_make_tables(L, ...). */
+int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E,
+                     const int *kind, const double *params, const double *coef,
+                     const double *wgrid, const double *tables, double *out, int *status,
+                     void *workspace, size_t workspace_bytes, void *stream);
+
+/* Same computation with HOST inputs and HOST output (the reference's
+ * calling convention: numpy in, numpy out).  Copies inputs in, integrates in
+ * device-sized chunks and streams the packed triangles back, overlapping the
+ * device->host copies with the next chunk's integration.  `out` should be
+ * page-locked for full copy bandwidth.  status may be NULL.  Synchronous. */
+int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, int E,
+                          const int *kind, const double *params, const double *coef,
+                          double *out, int *status);
+
+/* Expand packed upper triangles [E][N(N+1)/2] into full symmetric
+ * matrices [E][N][N] on the device (the reference's GramResult.matrix
+ * layout, gram.py:53-56, mirrored as _kernels.py:161-174 does). */
+int hxg_expand_full(int N, int E, const double *packed, double *full, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEXGRAM_B200_H */

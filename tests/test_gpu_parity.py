@@ -1,0 +1,253 @@
+"""Parity of the sm_100a kernels (through the C ABI) with the CPU oracle and
+the reference's golden vectors.  Tolerance: relative Frobenius error per
+element matrix <= 1e-12 (BASELINE.json north_star), fp64."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+SPACES = ("H1", "Hcurl", "Hdiv", "L2")
+
+
+def rel_fro(got_packed, ref_packed, N, orc):
+    G = orc.unpack(got_packed, N)
+    R = orc.unpack(ref_packed, N)
+    return np.linalg.norm(G - R) / np.linalg.norm(R)
+
+
+def check_batch(space, path, orders, L, b, orc, rule_order=None):
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import dim
+
+    packed, status = gram_batched(space, orders, b.kind, b.params, b.coef, path=path,
+                                  rule_order=L)
+    torch.cuda.synchronize()
+    got = packed.cpu().numpy()
+    ref = orc.gram_batched(space, path, orders, L, b.kind, b.params, b.coef)
+    N = dim(space, orders)
+    worst = max(rel_fro(got[e], ref[e], N, orc) for e in range(b.size))
+    assert worst <= TOL, (space, path, orders, L, worst)
+    assert int(status.abs().sum()) == 0
+    return worst
+
+
+@pytest.mark.parametrize("space", SPACES)
+@pytest.mark.parametrize("orders", [(1, 1, 1), (2, 2, 2), (2, 3, 2), (1, 2, 3), (3, 2, 3),
+                                    (2, 3, 4), (4, 4, 4)])
+def test_general_vs_oracle(space, orders, orc):
+    from paper_1711_00984_b200.inputs import trilinear_batch
+
+    b = trilinear_batch(5, 100 + sum(orders), variable_coef=True)
+    check_batch(space, "general", orders, max(orders) + 1, b, orc)
+
+
+@pytest.mark.parametrize("space", SPACES)
+@pytest.mark.parametrize("orders", [(1, 1, 1), (2, 2, 2), (3, 2, 3), (1, 2, 3), (4, 4, 4)])
+def test_affine_vs_oracle(space, orders, orc):
+    from paper_1711_00984_b200.inputs import affine_batch
+
+    b = affine_batch(5, 200 + sum(orders), variable_coef=True)
+    check_batch(space, "affine", orders, 1, b, orc)
+
+
+@pytest.mark.parametrize("space", SPACES)
+@pytest.mark.parametrize("p", [5, 6, 7, 8, 9, 10])
+def test_high_order_general(space, p, orc):
+    """Sweep orders (config 5): includes L > 8 (second kernel instantiation)
+    and n1 > 8 (two DMMA row tiles)."""
+    from paper_1711_00984_b200.inputs import trilinear_batch
+
+    b = trilinear_batch(2, 300 + p)
+    check_batch(space, "general", (p, p, p), p + 1, b, orc)
+
+
+@pytest.mark.parametrize("space", SPACES)
+@pytest.mark.parametrize("p", [6, 8, 10, 12])
+def test_high_order_affine(space, p, orc):
+    from paper_1711_00984_b200.inputs import affine_batch
+
+    b = affine_batch(3, 400 + p)
+    check_batch(space, "affine", (p, p, p), 1, b, orc)
+
+
+def test_golden_cases_dropin_api(golden):
+    """The reference's own matrices through the drop-in per-element API."""
+    import paper_1711_00984_b200 as hx
+
+    for c in golden_cases(golden):
+        sig = hx.SpaceSignature(c["space"], c["orders"])
+        kind_name = {0: "identity", 1: "diagonal-affine", 2: "general-affine", 3: "extrusion",
+                     4: "trilinear"}[c["kind"]]
+        em = hx.ElementMap(kind_name, c["params"])
+        if c["path"] == "affine":
+            res = hx.gram_simplified(sig, em, mass_weight=c["coef"])
+        elif c["wgrid"] is not None:
+            w = lambda x: 1.0 + x[0] ** 2 + 0.5 * x[1]  # noqa: E731 (make_golden.py)
+            res = hx.gram_tensorized(sig, em, hx.gauss_rule(c["L"]), "alternative",
+                                     mass_weight=w)
+        else:
+            res = hx.gram_tensorized(sig, em, hx.gauss_rule(c["L"]), "alternative",
+                                     mass_weight=c["coef"])
+        N = res.matrix.shape[0]
+        R = np.zeros((N, N))
+        iu = np.triu_indices(N)
+        R[iu] = c["packed"]
+        R.T[iu] = c["packed"]
+        rel = np.linalg.norm(res.matrix - R) / np.linalg.norm(R)
+        assert rel <= TOL, (c["space"], c["path"], c["orders"], kind_name, rel)
+        np.testing.assert_array_equal(res.matrix, res.matrix.T)
+        assert res.counters.accumulations == c["acc"]
+
+
+@pytest.mark.parametrize("name", ["c1_h1_p3_affine", "c2_h1_p5_general", "c3_hcurl_p6_general",
+                                  "c3_hcurl_p6_affine", "c4_hdiv_p7_general", "c4_l2_p7_general"])
+def test_config_golden_samples(golden, name):
+    """BASELINE config batches against the reference's own sampled entries."""
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import WORKLOADS
+
+    wl = WORKLOADS[name]
+    nel = 8 if name == "c1_h1_p3_affine" else 1
+    b = wl.batch(max(nel, 4))
+    packed, _ = gram_batched(wl.space, wl.orders, b.kind, b.params, b.coef, path=wl.path,
+                             rule_order=wl.L)
+    torch.cuda.synchronize()
+    got = packed.cpu().numpy()
+    for e in range(nel):
+        pre = f"{name}_e{e}"
+        if pre + "_packed" in golden.files:
+            ref = golden[pre + "_packed"]
+            vals, gv = ref, got[e]
+        else:
+            vals, gv = golden[pre + "_val"], got[e][golden[pre + "_idx"]]
+        fro = golden[pre + "_fro"][0]
+        assert np.linalg.norm(gv - vals) <= TOL * fro
+
+
+def test_full_config_batches(orc):
+    """Full BASELINE batch sizes: every element checked against the oracle on
+    a strided sample, plus size-independent properties on all elements
+    (finite, diagonal > 0)."""
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import WORKLOADS, dim
+
+    for name, wl in WORKLOADS.items():
+        b = wl.batch()
+        packed, status = gram_batched(wl.space, wl.orders, b.kind, b.params, b.coef,
+                                      path=wl.path, rule_order=wl.L)
+        torch.cuda.synchronize()
+        assert int(status.abs().sum()) == 0
+        N = dim(wl.space, wl.orders)
+        assert bool(torch.isfinite(packed).all())
+        diag_idx = torch.tensor([r * N - r * (r - 1) // 2 for r in range(N)], device=packed.device)
+        assert bool((packed[:, diag_idx] > 0).all())
+        sample = sorted(set([0, b.size - 1] + list(range(0, b.size, max(1, b.size // 6)))))[:8]
+        ref = orc.gram_batched(wl.space, wl.path, wl.orders, wl.L, b.kind[sample],
+                               b.params[sample], b.coef[sample])
+        got = packed[sample].cpu().numpy()
+        for k in range(len(sample)):
+            assert rel_fro(got[k], ref[k], N, orc) <= TOL, (name, sample[k])
+        del packed
+
+
+def test_general_equals_affine_on_affine_maps():
+    """Cross-path consistency (test_gram.py:145-153 pattern): on constant-
+    Jacobian maps the O(p^7) and O(p^6) kernels agree to 1e-12."""
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import affine_batch
+
+    for space in SPACES:
+        for p in (3, 6):
+            b = affine_batch(16, 500 + p, variable_coef=True)
+            g, _ = gram_batched(space, (p, p, p), b.kind, b.params, b.coef, path="general",
+                                rule_order=p + 1)
+            a, _ = gram_batched(space, (p, p, p), b.kind, b.params, b.coef, path="affine")
+            torch.cuda.synchronize()
+            num = torch.linalg.norm(g - a, dim=1)
+            den = torch.linalg.norm(a, dim=1)
+            assert float((num / den).max()) <= TOL, (space, p)
+
+
+def test_mass_weight_linearity():
+    """The coefficient multiplies only the mass term (test_gram.py:231-238)."""
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import trilinear_batch
+
+    b = trilinear_batch(4, 600)
+    for space in SPACES:
+        c0 = np.zeros(4)
+        c1 = np.ones(4)
+        c3 = np.full(4, 3.0)
+        g0, _ = gram_batched(space, (3, 3, 3), b.kind, b.params, c0)
+        g1, _ = gram_batched(space, (3, 3, 3), b.kind, b.params, c1)
+        g3, _ = gram_batched(space, (3, 3, 3), b.kind, b.params, c3)
+        torch.cuda.synchronize()
+        lhs = g3 - g0
+        rhs = 3.0 * (g1 - g0)
+        assert float(torch.linalg.norm(lhs - rhs) / torch.linalg.norm(g1)) <= 1e-13
+
+
+def test_edge_cases():
+    import torch
+
+    import paper_1711_00984_b200 as hx
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import trilinear_batch
+
+    # empty batch
+    b = trilinear_batch(1, 1)
+    out, st = gram_batched("H1", (2, 2, 2), b.kind[:0], b.params[:0], b.coef[:0])
+    assert out.shape == (0, 27 * 28 // 2)
+    # unsupported order -> InvalidOrderError
+    with pytest.raises(hx.InvalidOrderError):
+        gram_batched("H1", (13, 2, 2), b.kind, b.params, b.coef)
+    # trilinear kind on the affine path -> SimplificationNotApplicableError
+    with pytest.raises(hx.SimplificationNotApplicableError):
+        gram_batched("H1", (2, 2, 2), b.kind, b.params, b.coef, path="affine")
+    with pytest.raises(hx.SimplificationNotApplicableError):
+        hx.gram_simplified(hx.SpaceSignature("L2", (2, 2, 2)), hx.preset_map("trilinear"))
+    # inverted element -> DegenerateMapError from the device status word
+    par = b.params.copy().reshape(1, 8, 3)
+    par[0, :, 0] = 1.0 - par[0, :, 0]  # mirror x: det < 0 everywhere
+    with pytest.raises(hx.DegenerateMapError):
+        gram_batched("H1", (2, 2, 2), b.kind, par.reshape(1, 24), b.coef)
+    # L2 with the reference's default rule (L = max p) and loop-order counters
+    sig = hx.SpaceSignature("L2", (3, 3, 3))
+    r_std = hx.gram_tensorized(sig, hx.preset_map("trilinear"))
+    r_alt = hx.gram_tensorized(sig, hx.preset_map("trilinear"), loop_order="alternative")
+    np.testing.assert_array_equal(r_std.matrix, r_alt.matrix)
+    assert r_std.counters.geometry_calls > r_alt.counters.geometry_calls
+    torch.cuda.synchronize()
+
+
+def test_host_entry_matches_device_entry():
+    """hxg_gram_batched_host (host buffers, chunked, overlapped D2H) equals
+    the device entry."""
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.engine import get_engine
+    from paper_1711_00984_b200.inputs import packed_size, trilinear_batch
+
+    b = trilinear_batch(40, 700, variable_coef=True)
+    d, _ = gram_batched("Hcurl", (4, 4, 4), b.kind, b.params, b.coef)
+    out = torch.empty((40, packed_size("Hcurl", (4, 4, 4))), dtype=torch.float64).pin_memory()
+    status = np.zeros(40, np.int32)
+    get_engine().integrate_host("Hcurl", "general", (4, 4, 4), 5, b.kind, b.params, b.coef,
+                                out, status)
+    np.testing.assert_array_equal(out.numpy(), d.cpu().numpy())
+    assert status.sum() == 0
