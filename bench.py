@@ -1,0 +1,477 @@
+"""Benchmark of the batched Gram integration (BASELINE.json metric: Gram
+elements/s per space & test order, achieved fraction of the FP64/HBM
+roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+A step is one pass of the hot path over one synthetic batch of the
+workload (default: BASELINE configs[1], H1 Gram, trilinear maps, p_test=5,
+4096 elements per GPU).  Elements are sharded across ranks (weak scaling:
+each rank integrates its own slice of a seeded global batch; no collective on
+the data path).  Rank 0 prints one JSON line.
+
+--impl reference times the reference's CPU algorithm on the host cores (the
+C restatement in oracle/, pinned bit-exact to the reference package) on the
+same workload, metric and unit.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1711_00984_b200.inputs import WORKLOADS, dim  # noqa: E402
+
+METRIC = "Gram elements/sec per space & test order; achieved % of FP64/HBM roofline"
+UNIT = "elements/s"
+L2_BYTES = 126 * 2 ** 20
+PEAK_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "peaks_r01.jsonl")
+NCU_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def algorithmic(space, orders, path, L):
+    """Per element: F = 2 x reference accumulations, B = packed fp64 output
+    bytes."""
+    from paper_1711_00984_b200.gram import counters
+
+    N = dim(space, orders)
+    P = N * (N + 1) // 2
+    c = counters(space, orders, "tensorized" if path == "general" else "simplified",
+                 L if path == "general" else None)
+    return 2.0 * c.accumulations, 8.0 * P, P
+
+
+def peaks():
+    hbm = 6650.0
+    src_hbm = "fallback (B200_PROFILING.md)"
+    if os.path.exists(PEAK_FILE):
+        with open(PEAK_FILE) as fh:
+            hbm = float(json.load(fh)["hbm_gbs"])
+        src_hbm = "MEASURED_PEAKS.json hbm_gbs"
+    fp64 = 37.0
+    src_fp64 = "profiles/peaks_r01.jsonl dmma_m8n8k4 (measured on this pool's B200)"
+    if os.path.exists(FP64_PEAK_FILE):
+        with open(FP64_PEAK_FILE) as fh:
+            vals = [json.loads(l) for l in fh if l.strip()]
+        dm = [v["tflops"] for v in vals if v.get("test", "").startswith("dmma")]
+        if dm:
+            fp64 = max(dm)
+    return hbm, src_hbm, fp64, src_fp64
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.tmp = None
+
+    def __enter__(self):
+        try:
+            self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.tmp.flush()
+        with open(self.tmp.name) as fh:
+            rows = [r.strip().split(",") for r in fh if r.strip()]
+        os.unlink(self.tmp.name)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def max_over_ranks(x, world, device=None):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def shard(E, world, rank):
+    """Contiguous even element ranges [r E / n, (r+1) E / n)."""
+    lo = (rank * E) // world
+    hi = ((rank + 1) * E) // world
+    return lo, hi
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = C restatement of the reference, test infrastructure)
+# ---------------------------------------------------------------------------
+def cpu_rate(wl, seconds, nthreads=0):
+    """Elements/s of the reference algorithm on the host cores over a bounded
+    sample (>= `seconds` of work, starting at 64 elements and doubling)."""
+    from oracle import oracle
+
+    threads = nthreads or oracle.num_cpus()
+    b = wl.batch(64)
+    L = wl.L if wl.path == "general" else 1
+    oracle.gram_batched(wl.space, wl.path, wl.orders, L, b.kind[:threads], b.params[:threads],
+                        b.coef[:threads], nthreads=threads)  # warm
+    n = max(threads, 8)
+    while True:
+        bb = wl.batch(n)
+        t0 = time.perf_counter()
+        oracle.gram_batched(wl.space, wl.path, wl.orders, L, bb.kind, bb.params, bb.coef,
+                            nthreads=threads)
+        dt = time.perf_counter() - t0
+        if dt >= seconds or n >= 1 << 20:
+            return n / dt, n, dt, threads
+        n = int(n * min(8.0, max(2.0, 1.2 * seconds / max(dt, 1e-3))))
+
+
+def run_reference(args, wl, world, rank):
+    if rank != 0:
+        return
+    from oracle import oracle
+
+    threads = oracle.num_cpus()
+    # size one step to ~2 s of host work
+    rate, _, _, _ = cpu_rate(wl, 1.0, threads)
+    per_step = max(threads, int(rate * 2.0))
+    b = wl.batch(per_step)
+    L = wl.L if wl.path == "general" else 1
+    for _ in range(args.warmup):
+        oracle.gram_batched(wl.space, wl.path, wl.orders, L, b.kind, b.params, b.coef,
+                            nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.gram_batched(wl.space, wl.path, wl.orders, L, b.kind, b.params, b.coef,
+                            nthreads=threads)
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    F, B, P = algorithmic(wl.space, wl.orders, wl.path, wl.L)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY 8(d))",
+        "config": {"workload": wl.name, "space": wl.space, "p_test": wl.p, "L": wl.L,
+                   "path": wl.path, "maps": wl.maps, "elements_per_step": per_step},
+        "gram_entries_per_s": value * P,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{per_step} elements per step of {wl.name}, "
+                                   f"oracle/hexgram_oracle.c (alternative loop order, "
+                                   f"pthreads over elements)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+class DeviceStep:
+    """One batch resident in HBM; step() launches the hot path on `stream`."""
+
+    def __init__(self, wl, E, lo, device):
+        import torch
+
+        from paper_1711_00984_b200 import _native
+        from paper_1711_00984_b200.engine import get_engine
+
+        self.wl = wl
+        self.E = E
+        self.torch = torch
+        self.eng = get_engine(device)
+        self.lib = _native.lib()
+        b = wl.batch(lo + E).slice(lo, lo + E)
+        self.host = b
+        dev = self.eng.device
+        self.kind = torch.as_tensor(b.kind).to(dev)
+        self.params = torch.as_tensor(b.params).to(dev)
+        self.coef = torch.as_tensor(b.coef).to(dev)
+        self.sc = _native.SPACE_CODES[wl.space]
+        self.L = wl.L if wl.path == "general" else 1
+        N = dim(wl.space, wl.orders)
+        self.P = N * (N + 1) // 2
+        self.out = torch.empty((E, self.P), dtype=torch.float64, device=dev)
+        self.status = torch.zeros(E, dtype=torch.int32, device=dev)
+        self.tab = self.eng.tables(self.L)
+        ws = self.lib.hxg_workspace_size(self.sc, 0 if wl.path == "general" else 1,
+                                         *wl.orders, self.L, E)
+        self.ws_bytes = ws
+        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+        self.full_metric = ws >= self.lib.hxg_workspace_size(self.sc, 0, *wl.orders, self.L, E) \
+            if wl.path == "general" else True
+        self.flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+        self.launches_per_step = 0
+
+    def _p(self, t):
+        return ctypes.c_void_p(t.data_ptr())
+
+    def flush(self):
+        self.flush_buf.fill_(1)
+
+    def step(self, stream, ev_mid=None):
+        wl, lib, s = self.wl, self.lib, ctypes.c_void_p(stream.cuda_stream)
+        if wl.path == "general" and ev_mid is not None and self.full_metric:
+            rc = lib.hxg_metric_batched(self.sc, *wl.orders, self.L, self.E, self._p(self.kind),
+                                        self._p(self.params), self._p(self.coef), None,
+                                        self._p(self.tab), self._p(self.ws), self._p(self.status), s)
+            assert rc == 0, rc
+            ev_mid.record(stream)
+            rc = lib.hxg_contract_batched(self.sc, *wl.orders, self.L, self.E, self._p(self.tab),
+                                          self._p(self.ws), self._p(self.out), s)
+            assert rc == 0, rc
+            self.launches_per_step = 2
+            return
+        if ev_mid is not None and wl.path == "affine":
+            ev_mid.record(stream)
+        rc = lib.hxg_gram_batched(self.sc, 0 if wl.path == "general" else 1, *wl.orders, self.L,
+                                  self.E, self._p(self.kind), self._p(self.params),
+                                  self._p(self.coef), None, self._p(self.tab), self._p(self.out),
+                                  self._p(self.status), self._p(self.ws), self.ws_bytes, s)
+        assert rc == 0, rc
+        if ev_mid is not None and wl.path == "general":
+            ev_mid.record(stream)
+        self.launches_per_step = 1 if wl.path == "affine" else 2
+
+
+def measure_device(wl, E, lo, steps, warmup, world, device, with_clocks=True):
+    import torch
+
+    ds = DeviceStep(wl, E, lo, device)
+    stream = torch.cuda.current_stream(device)
+    for _ in range(warmup):
+        ds.flush()
+        ds.step(stream)
+    torch.cuda.synchronize(device)
+    assert int(ds.status.abs().sum()) == 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    sampler = ClockSampler(device.index if device.index is not None else 0) if with_clocks else None
+    if sampler:
+        sampler.__enter__()
+    for k in range(steps):
+        ds.flush()  # L2 flush between timed iterations (outside the timed events)
+        ev[k][0].record(stream)
+        ds.step(stream, ev[k][1])
+        ev[k][2].record(stream)
+    torch.cuda.synchronize(device)
+    if sampler:
+        sampler.__exit__(None, None, None)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    step_ms = [a.elapsed_time(c) for a, b, c in ev]
+    kern_ms = [b.elapsed_time(c) for a, b, c in ev]
+    total_ms = sum(step_ms)
+    return ds, total_ms, kern_ms, (sampler.summary() if sampler else None)
+
+
+def measure_e2e(ds, steps, world, device):
+    """Through the C ABI with HOST buffers: inputs from host memory, packed
+    triangles back into pinned host memory, every step (hxg_gram_batched_host)."""
+    import torch
+
+    wl = ds.wl
+    out = torch.empty((ds.E, ds.P), dtype=torch.float64).pin_memory()
+    b = ds.host
+    kind = np.ascontiguousarray(b.kind)
+    params = np.ascontiguousarray(b.params)
+    coef = np.ascontiguousarray(b.coef)
+    ds.eng.integrate_host(wl.space, wl.path, wl.orders, ds.L, kind, params, coef, out)  # warm
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ds.eng.integrate_host(wl.space, wl.path, wl.orders, ds.L, kind, params, coef, out)
+    dt = time.perf_counter() - t0
+    dt = max_over_ranks(dt, world, device)
+    h2d = kind.nbytes + params.nbytes + coef.nbytes
+    d2h = ds.E * ds.P * 8
+    del out
+    return dt, h2d, d2h
+
+
+def run_ours(args, wl, world, rank, local):
+    import torch
+
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    E = args.elements or wl.E
+    lo, _ = shard(E * world, world, rank)
+    F, B, P = algorithmic(wl.space, wl.orders, wl.path, wl.L)
+    hbm, src_hbm, fp64, src_fp64 = peaks()
+
+    ds, total_ms, kern_ms, clocks = measure_device(wl, E, lo, args.steps, args.warmup, world,
+                                                   device)
+    total_ms = max_over_ranks(total_ms, world, device)
+    sec = total_ms / 1e3
+    value = E * world * args.steps / sec
+    # dominant kernel: the contraction kernel (general) / the affine kernel
+    kmean_s = statistics.mean(kern_ms) / 1e3
+    if wl.path == "general" and not ds.full_metric:
+        kmean_s = sec / args.steps  # chunked launches: whole step
+    t_f, t_b = E * F / (fp64 * 1e12), E * B / (hbm * 1e9)
+    bound = "tensor" if t_f >= t_b else "hbm"
+    traffic = None
+    if os.path.exists(NCU_TRAFFIC_FILE):
+        with open(NCU_TRAFFIC_FILE) as fh:
+            traffic = json.load(fh).get(wl.name)
+    if bound == "tensor":
+        achieved = E * F / kmean_s / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                "frac": achieved / fp64, "traffic": traffic,
+                "peak_source": src_fp64 + " (FP64 DMMA; no fp64 entry in MEASURED_PEAKS.json)"}
+    else:
+        achieved = E * B / kmean_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic, "peak_source": src_hbm}
+    roof.update({
+        "kernel": "general_kernel (hxg_contract_batched)" if wl.path == "general" else "affine_kernel",
+        "kernel_ms_per_launch": kmean_s * 1e3,
+        "algorithmic_flops_per_launch": E * F, "algorithmic_bytes_per_launch": E * B,
+        "flops_per_element": F, "bytes_per_element": B,
+        "roofline_model_frac": max(t_f, t_b) / (sec / args.steps),
+        "hbm_write_gbs": E * B / kmean_s / 1e9,
+        "fp64_tflops_alg": E * F / kmean_s / 1e12,
+    })
+    e2e_dt, h2d, d2h = measure_e2e(ds, args.e2e_steps or args.steps, world, device)
+    e2e_steps = args.e2e_steps or args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY 8(d)); random-init element maps",
+        "config": {"workload": wl.name, "space": wl.space, "p_test": wl.p, "L": wl.L,
+                   "path": wl.path, "maps": wl.maps, "elements_per_gpu": E,
+                   "global_elements": E * world, "N": dim(wl.space, wl.orders),
+                   "parallelism": f"element-shard x{world}",
+                   "l2": "flushed (256 MB write) between timed steps; output per step "
+                         f"{E * B / 2**20:.0f} MB"},
+        "gram_entries_per_s": value * P,
+        "roofline": roof,
+        "clocks": clocks,
+        "gpu_launches": ds.launches_per_step * args.steps,
+        "e2e": {"value": E * world * e2e_steps / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "api": "hxg_gram_batched_host (C ABI, host buffers, pinned output)"},
+    }
+    if args.suite and rank == 0 and world == 1:
+        suite = []
+        for name, w2 in WORKLOADS.items():
+            d2, tms, kms, _ = measure_device(w2, w2.E, 0, max(3, args.steps // 2), 2, 1, device,
+                                             with_clocks=False)
+            F2, B2, P2 = algorithmic(w2.space, w2.orders, w2.path, w2.L)
+            st = tms / 1e3 / max(3, args.steps // 2)
+            km = statistics.mean(kms) / 1e3 if d2.full_metric else st
+            tf2, tb2 = w2.E * F2 / (fp64 * 1e12), w2.E * B2 / (hbm * 1e9)
+            suite.append({"workload": name, "elements_per_s": w2.E / st,
+                          "gram_entries_per_s": w2.E * P2 / st, "ms_per_step": st * 1e3,
+                          "kernel_ms": km * 1e3, "roofline_frac": max(tf2, tb2) / st,
+                          "bound": "fp64" if tf2 >= tb2 else "hbm",
+                          "fp64_tflops_alg": w2.E * F2 / km / 1e12,
+                          "hbm_write_gbs": w2.E * B2 / km / 1e9})
+            del d2
+            torch.cuda.empty_cache()
+        line["suite"] = suite
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, n, dt, threads = cpu_rate(wl, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{n} elements of {wl.name} in {dt:.1f} s "
+                                          f"(oracle/hexgram_oracle.c, {threads} threads)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="c2_h1_p5_general", choices=sorted(WORKLOADS))
+    ap.add_argument("--elements", type=int, default=0, help="elements per GPU (default: config)")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--suite", action=argparse.BooleanOptionalAction, default=True)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl, world, rank)
+    else:
+        run_ours(args, wl, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

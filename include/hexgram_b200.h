@@ -98,6 +98,20 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E,
                      const double *wgrid, const double *tables, double *out, int *status,
                      void *workspace, size_t workspace_bytes, void *stream);
 
+/* The two stages of the general path, exported separately so callers can
+ * schedule / time them (hxg_gram_batched = metric + contract per chunk).
+ * hxg_metric_batched: per-point metric kernel, metric[E][nfields][L^3]
+ *   (Jacobian, det, D, C, weights and mass coefficient folded; _kernels.py:56-136
+ *   and the per-point weight folding of tens_*, e.g. _kernels.py:578-590).
+ *   metric must hold hxg_workspace_size(space, 0, p.., L, E) bytes for this E.
+ * hxg_contract_batched: three-stage sum-factorized contraction + packed output
+ *   writer (stages A/B/C of tens_*_alt, _kernels.py:541-624, 742-853, 1003-1150). */
+int hxg_metric_batched(int space, int p1, int p2, int p3, int L, int E, const int *kind,
+                       const double *params, const double *coef, const double *wgrid,
+                       const double *tables, double *metric, int *status, void *stream);
+int hxg_contract_batched(int space, int p1, int p2, int p3, int L, int E, const double *tables,
+                         const double *metric, double *out, void *stream);
+
 /* Same computation with HOST inputs and HOST output (the reference's
  * calling convention: numpy in, numpy out).  Copies inputs in, integrates in
  * device-sized chunks and streams the packed triangles back, overlapping the

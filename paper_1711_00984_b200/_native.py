@@ -38,6 +38,8 @@ EXPORTED = (
     "hxg_make_tables",
     "hxg_workspace_size",
     "hxg_gram_batched",
+    "hxg_metric_batched",
+    "hxg_contract_batched",
     "hxg_gram_batched_host",
     "hxg_expand_full",
 )
@@ -83,6 +85,10 @@ def lib():
     L.hxg_gram_batched.argtypes = [_i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                    _vp, _sz, _vp]
     L.hxg_gram_batched.restype = _i
+    L.hxg_metric_batched.argtypes = [_i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.hxg_metric_batched.restype = _i
+    L.hxg_contract_batched.argtypes = [_i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp]
+    L.hxg_contract_batched.restype = _i
     L.hxg_gram_batched_host.argtypes = [_i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]
     L.hxg_gram_batched_host.restype = _i
     L.hxg_expand_full.argtypes = [_i, _i, _vp, _vp, _vp]

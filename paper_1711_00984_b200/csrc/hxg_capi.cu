@@ -395,14 +395,56 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
         return HXG_OK;
     }
 
-    // general path
+    // general path: metric kernel then the three-stage contraction, per chunk
     if (!workspace) return HXG_ERR_WORKSPACE;
     const int Ech = elements_per_chunk(P, L, E, workspace_bytes);
     if (Ech < 1) return HXG_ERR_WORKSPACE;
+    for (long long e0 = 0; e0 < E; e0 += Ech) {
+        const int ne = (int)std::min<long long>(Ech, E - e0);
+        double *metric = (double *)workspace;
+        rc = hxg_metric_batched(space, p1, p2, p3, L, ne, kind + e0, params + 24 * e0,
+                                coef ? coef + e0 : nullptr, wgrid ? wgrid + e0 * L * L * L : nullptr,
+                                tables, metric, status + e0, stream);
+        if (rc != HXG_OK) return rc;
+        rc = hxg_contract_batched(space, p1, p2, p3, L, ne, tables, metric, out + e0 * Pk, stream);
+        if (rc != HXG_OK) return rc;
+    }
+    return HXG_OK;
+}
+
+int hxg_metric_batched(int space, int p1, int p2, int p3, int L, int E, const int *kind,
+                       const double *params, const double *coef, const double *wgrid,
+                       const double *tables, double *metric, int *status, void *stream)
+{
+    int rc = check_common(space, GENERAL, p1, p2, p3, L, E);
+    if (rc != HXG_OK) return rc;
+    if (E == 0) return HXG_OK;
+    if (!kind || !params || !tables || !metric || !status) return HXG_ERR_ARG;
+    SpacePlan P;
+    rc = build_plan(space, p1, p2, p3, P);
+    if (rc != HXG_OK) return rc;
+    const long long npts = (long long)E * L * L * L;
+    const int mgrid = (int)std::min<long long>((npts + 255) / 256, 148LL * 64);
+    metric_kernel<<<mgrid, 256, 0, (cudaStream_t)stream>>>(space, L, E, kind, params, coef, wgrid,
+                                                         tables, metric, status, P.nfields);
+    return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
+}
+
+int hxg_contract_batched(int space, int p1, int p2, int p3, int L, int E, const double *tables,
+                         const double *metric, double *out, void *stream)
+{
+    int rc = check_common(space, GENERAL, p1, p2, p3, L, E);
+    if (rc != HXG_OK) return rc;
+    if (E == 0) return HXG_OK;
+    if (!tables || !metric || !out) return HXG_ERR_ARG;
+    SpacePlan P;
+    rc = build_plan(space, p1, p2, p3, P);
+    if (rc != HXG_OK) return rc;
     GenArgs g;
     memset(&g, 0, sizeof(g));
     g.plan = P;
     g.L = L;
+    g.E = E;
     const GenConfig cfg = gen_config(P, L, GEN_SMEM_BUDGET);
     if (cfg.smem > GEN_SMEM_MAX) return HXG_ERR_ORDER;
     g.LP = cfg.LP;
@@ -417,8 +459,9 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
     g.off_B = cfg.off_B;
     g.off_S = cfg.off_S;
     g.tables = tables;
-    g.P = Pk;
-    // work units ordered heaviest first inside an element (longest packed rows)
+    g.metric = metric;
+    g.out = out;
+    g.P = (long long)P.N * (P.N + 1) / 2;
     int nu = 0;
     for (int b = 0; b < P.nb; ++b)
         for (int j3 = 0; j3 < P.n[b][2]; ++j3) {
@@ -430,29 +473,14 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
     int n1max = 0;
     for (int a = 0; a < P.nb; ++a) n1max = std::max(n1max, P.n[a][0]);
     const int nmt = n1max <= 8 ? 1 : 2;
-    for (long long e0 = 0; e0 < E; e0 += Ech) {
-        const int ne = (int)std::min<long long>(Ech, E - e0);
-        double *metric = (double *)workspace;
-        const long long npts = (long long)ne * L * L * L;
-        const int mgrid = (int)std::min<long long>((npts + 255) / 256, 148LL * 64);
-        metric_kernel<<<mgrid, 256, 0, st>>>(space, L, ne, kind + e0, params + 24 * e0,
-                                             coef ? coef + e0 : nullptr,
-                                             wgrid ? wgrid + e0 * L * L * L : nullptr, tables,
-                                             metric, status + e0, P.nfields);
-        if (cudaGetLastError() != cudaSuccess) return HXG_ERR_CUDA;
-        GenArgs c = g;
-        c.E = ne;
-        c.metric = metric;
-        c.out = out + e0 * Pk;
-        const long long grid = (long long)ne * nu;
-        if (grid >= (1ll << 31)) return HXG_ERR_ARG;
-        if (L <= 8) rc = nmt == 1 ? launch_general_t<8, 1>(c, cfg.smem, (int)grid, st)
-                                  : launch_general_t<8, 2>(c, cfg.smem, (int)grid, st);
-        else rc = nmt == 1 ? launch_general_t<16, 1>(c, cfg.smem, (int)grid, st)
-                           : launch_general_t<16, 2>(c, cfg.smem, (int)grid, st);
-        if (rc != HXG_OK) return rc;
-    }
-    return HXG_OK;
+    const long long grid = (long long)E * nu;
+    if (grid >= (1ll << 31)) return HXG_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (L <= 8) rc = nmt == 1 ? launch_general_t<8, 1>(g, cfg.smem, (int)grid, st)
+                              : launch_general_t<8, 2>(g, cfg.smem, (int)grid, st);
+    else rc = nmt == 1 ? launch_general_t<16, 1>(g, cfg.smem, (int)grid, st)
+                       : launch_general_t<16, 2>(g, cfg.smem, (int)grid, st);
+    return rc;
 }
 
 int hxg_expand_full(int N, int E, const double *packed, double *full, void *stream)
