@@ -53,7 +53,7 @@ _sz = ctypes.c_size_t
 
 def build(force: bool = False) -> str:
     """Compile the CUDA library with the in-tree Makefile (nvcc, sm_100a)."""
-    cmd = ["make", "-s", "-C", CSRC]
+    cmd = ["make", "-s", f"-j{min(8, os.cpu_count() or 1)}", "-C", CSRC]
     if force:
         cmd.insert(1, "-B")
     subprocess.run(cmd, check=True)

@@ -8,7 +8,10 @@
 #include <vector>
 
 #include "../../include/hexgram_b200.h"
+#include "hxg_general_v2.cuh"
 #include "hxg_kernels.cuh"
+#include "hxg_v2_launch.h"
+#include <cstdlib>
 
 using namespace hxg;
 
@@ -440,6 +443,26 @@ int hxg_contract_batched(int space, int p1, int p2, int p3, int L, int E, const 
     SpacePlan P;
     rc = build_plan(space, p1, p2, p3, P);
     if (rc != HXG_OK) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    // compile-time specialized kernels: isotropic p <= 10 with L = p + 1
+    // (HXG_FORCE_GENERIC=1 selects the runtime-generic kernel, for testing)
+    const char *force = getenv("HXG_FORCE_GENERIC");
+    if (p1 == p2 && p2 == p3 && L == p1 + 1 && !(force && force[0] == '1')) {
+        V2Args a;
+        a.tables = tables;
+        a.metric = metric;
+        a.out = out;
+        a.P = (long long)P.N * (P.N + 1) / 2;
+        a.E = E;
+        int r = 1;
+        switch (space) {
+        case H1: r = launch_v2_H1(p1, a, st); break;
+        case HCURL: r = launch_v2_hcurl(p1, a, st); break;
+        case HDIV: r = launch_v2_hdiv(p1, a, st); break;
+        case L2: r = launch_v2_l2(p1, a, st); break;
+        }
+        if (r <= 0) return r == 0 ? HXG_OK : HXG_ERR_CUDA;
+    }
     GenArgs g;
     memset(&g, 0, sizeof(g));
     g.plan = P;
@@ -475,7 +498,6 @@ int hxg_contract_batched(int space, int p1, int p2, int p3, int L, int E, const 
     const int nmt = n1max <= 8 ? 1 : 2;
     const long long grid = (long long)E * nu;
     if (grid >= (1ll << 31)) return HXG_ERR_ARG;
-    cudaStream_t st = (cudaStream_t)stream;
     if (L <= 8) rc = nmt == 1 ? launch_general_t<8, 1>(g, cfg.smem, (int)grid, st)
                               : launch_general_t<8, 2>(g, cfg.smem, (int)grid, st);
     else rc = nmt == 1 ? launch_general_t<16, 1>(g, cfg.smem, (int)grid, st)

@@ -1,0 +1,33 @@
+// Specialized general-map kernels for space HDIV, isotropic orders p = 1..10, L = p + 1.
+#include "hxg_general_v2.cuh"
+#include "hxg_v2_launch.h"
+
+namespace hxg {
+
+template <int P>
+static int launch_one(const V2Args &a, int grid, cudaStream_t st)
+{
+    using C = V2Cfg<HDIV, P, P + 1>;
+    auto k = general_v2_kernel<HDIV, P, P + 1>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
+        return -5;
+    k<<<grid, GEN_THREADS, C::SMEM_BYTES, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+template <int P>
+static int units_one() { return V2Cfg<HDIV, P, P + 1>::NU; }
+
+// returns 1 if no specialization exists for p, else 0 / negative error
+int launch_v2_hdiv(int p, const V2Args &a, cudaStream_t st)
+{
+    switch (p) {
+#define HXG_CASE(PP) case PP: return launch_one<PP>(a, a.E * units_one<PP>(), st);
+        HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
+        HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#undef HXG_CASE
+    }
+    return 1;
+}
+
+}  // namespace hxg

@@ -1,0 +1,382 @@
+// hxg_general_v2.cuh -- compile-time specialized general-map Gram kernel.
+//
+// Same three-stage sum factorization as general_kernel (hxg_kernels.cuh), with
+// the space, the (isotropic) order p and the rule size L as template
+// parameters, so every extent, term list, group list and index division is a
+// compile-time constant and all stage loops unroll.  One CTA integrates one
+// work unit (element e, trial block b, test block a >= b, trial digit j3): the
+// block-(a) columns of the packed rows J = (j1, j2, j3, b).
+//
+// Stage C (contraction over xi1) runs on FP64 DMMA (mma.sync m8n8k4) in one of
+// two factorizations, chosen per block pair at compile time by FP64-pipe cost
+// (DMMA and DFMA share the FP64 pipe on B200; profiles/peaks_r01.jsonl):
+//   B-form: D[j1, (i1,i2,i3)] = sum_{h,l} u_s(j1,l) * (u_r(i1,l) B_h[i2,i3,l])
+//           A operand = trial 1D table (registers), B operand = table x B_h
+//   Y-form: D[j1, i1] (per (i2,i3)) = sum_{r,l} Y_r[j1,l] u_r(i1,l),
+//           Y_r[j1,l] = sum_{h: r(h)=r} u_s(h)(j1,l) B_h[l]  (built per fragment)
+// The Y-form needs about nr*L FMAs per Gram entry instead of nh*L (H1: 2L vs
+// 4L), at the price of 8x8 output tiles that span only n1a x n1b entries.
+#pragma once
+#include "hxg_common.cuh"
+#include "hxg_terms.h"
+
+namespace hxg {
+
+struct V2Args {
+    const double *tables;  // TAB_TOTAL
+    const double *metric;  // [E][nfields][n][l][m]
+    double *out;           // [E][P]
+    long long P;
+    int E;
+};
+
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+
+template <int S, int P, int L>
+struct V2Cfg {
+    static constexpr int NB = nb_of(S);
+    static constexpr int LP = (L + 1) & ~1;
+    static constexpr int NF = nf_of(S);
+    static constexpr int L3 = L * L * L;
+    __host__ __device__ static constexpr int n(int a, int d) { return ext_of(S, P, a, d); }
+    __host__ __device__ static constexpr int nmax(int d)
+    {
+        return cmax(n(0, d), NB > 1 ? cmax(n(1, d), n(2, d)) : 0);
+    }
+    __host__ __device__ static constexpr int off(int a)
+    {
+        return a == 0 ? 0 : (a == 1 ? n(0, 0) * n(0, 1) * n(0, 2)
+                                    : n(0, 0) * n(0, 1) * n(0, 2) + n(1, 0) * n(1, 1) * n(1, 2));
+    }
+    static constexpr int N = off(NB - 1) + n(NB - 1, 0) * n(NB - 1, 1) * n(NB - 1, 2);
+    static constexpr int N1 = nmax(0), N2 = nmax(1), N3 = nmax(2);
+    __host__ __device__ static constexpr int c12(int a) { return n(a, 0) * n(a, 1); }
+    static constexpr int C12 = cmax(c12(0), NB > 1 ? cmax(c12(1), c12(2)) : 0);
+    __host__ __device__ static constexpr int maxg()
+    {
+        int m = 1;
+        for (int a = 0; a < NB; ++a)
+            for (int b = 0; b < NB; ++b) m = cmax(m, make_pair_plan(S, a, b).ng);
+        return m;
+    }
+    __host__ __device__ static constexpr int maxh()
+    {
+        int m = 1;
+        for (int a = 0; a < NB; ++a)
+            for (int b = 0; b < NB; ++b) m = cmax(m, make_pair_plan(S, a, b).nh);
+        return m;
+    }
+    static constexpr int NG = maxg(), NH = maxh();
+    static constexpr int BUDGET = (110 * 1024) / 8;  // doubles: 2 CTAs per SM
+    __host__ __device__ static constexpr int sld(int R3) { return ((C12 * R3 + 7) / 8) * 8 + 2; }
+    __host__ __device__ static constexpr int smem(int R2, int R3)
+    {
+        return 2 * KT * LP + R3 * NG * L * LP + R2 * NH * R3 * N2 * LP + R2 * N1 * sld(R3);
+    }
+    __host__ __device__ static constexpr int pick_r3()
+    {
+        for (int r = N3; r >= 1; --r)
+            if (smem(N2, r) <= BUDGET) return r;
+        return 1;
+    }
+    static constexpr int R3 = pick_r3();
+    __host__ __device__ static constexpr int pick_r2()
+    {
+        for (int r = N2; r >= 1; --r)
+            if (smem(r, R3) <= BUDGET) return r;
+        return 1;
+    }
+    static constexpr int R2 = pick_r2();
+    static constexpr int SLD = sld(R3);
+    static constexpr int OFF_T = 0;
+    static constexpr int OFF_A = OFF_T + 2 * KT * LP;
+    static constexpr int OFF_B = OFF_A + R3 * NG * L * LP;
+    static constexpr int OFF_S = OFF_B + R2 * NH * R3 * N2 * LP;
+    static constexpr int SMEM_BYTES = smem(R2, R3) * 8;
+    static constexpr int SJ2 = NH * R3 * N2 * LP;  // sB stride per j2
+    static constexpr int SH = R3 * N2 * LP;        // sB stride per h
+    __host__ __device__ static constexpr int units()
+    {
+        int u = 0;
+        for (int b = 0; b < NB; ++b) u += (NB - b) * n(b, 2);
+        return u;
+    }
+    static constexpr int NU = units();
+    static constexpr int MINB = SMEM_BYTES <= 113 * 1024 ? 2 : 1;
+
+    // stage-C factorization per block pair (see file header)
+    __host__ __device__ static constexpr bool yform(int a, int b)
+    {
+        const CPair pp = make_pair_plan(S, a, b);
+        if (n(a, 0) > 8 || n(b, 0) > 8) return false;
+        const int costB8 = n(a, 0) * ((pp.nh * L + 3) / 4) * 288;
+        int costY = 0;
+        for (int r = 0; r < pp.nr; ++r) {
+            int hr = 0;
+            for (int h = 0; h < pp.nh; ++h) hr += pp.h_r[h] == r;
+            costY += ((L + 3) / 4) * (256 + 32 * hr);
+        }
+        return 8 * costY < costB8;
+    }
+};
+
+__device__ __forceinline__ void st_cs(double *p, double v) { __stcs(p, v); }
+
+template <int S, int P, int L, int A, int B>
+__device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int e, int j3)
+{
+    using C = V2Cfg<S, P, L>;
+    constexpr CPair pp = make_pair_plan(S, A, B);
+    constexpr int LP = C::LP, L3 = C::L3, NG = C::NG, N2 = C::N2, R2 = C::R2, R3 = C::R3;
+    constexpr int SLD = C::SLD, SJ2 = C::SJ2, SH = C::SH, N = C::N;
+    constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1), n3a = C::n(A, 2);
+    constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1);
+    constexpr int sha0 = sh_of(S, A, 0), sha1 = sh_of(S, A, 1), sha2 = sh_of(S, A, 2);
+    constexpr int shb0 = sh_of(S, B, 0), shb1 = sh_of(S, B, 1), shb2 = sh_of(S, B, 2);
+    constexpr int offA = C::off(A), offB = C::off(B);
+    constexpr bool YF = C::yform(A, B);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const double *sT = smem + C::OFF_T;
+    double *sA = smem + C::OFF_A;
+    double *sB = smem + C::OFF_B;
+    double *sS = smem + C::OFF_S;
+    const double *__restrict__ M = args.metric + (long long)e * C::NF * L3;
+    double *__restrict__ outE = args.out + (long long)e * args.P;
+
+    // ---- per-CTA stage-C operand registers ---------------------------------
+    constexpr int KD = pp.nh * L;
+    constexpr int NKS = (KD + 3) / 4;          // B-form k-steps
+    constexpr int NMT = (n1b + 7) / 8;         // B-form row tiles
+    constexpr int LQ = (L + 3) / 4;            // Y-form k-steps per r segment
+    constexpr int KSY = pp.nr * LQ;            // Y-form k-steps
+    constexpr int NKR = YF ? 1 : NKS;          // register array extents
+    constexpr int NYR = YF ? KSY : 1;
+    double Af[NMT][NKR];
+    double Yb[NYR];
+    double Yc[NYR][2];
+    int Yl[NYR];
+    (void)Af; (void)Yb; (void)Yc; (void)Yl;
+    if constexpr (!YF) {
+#pragma unroll
+        for (int mt = 0; mt < NMT; ++mt)
+#pragma unroll
+            for (int ks = 0; ks < NKS; ++ks) {
+                const int j1 = mt * 8 + g8, k = ks * 4 + t4;
+                const int h = k / L, l = k - h * L;
+                int fs = 0;
+#pragma unroll
+                for (int hh = 0; hh < pp.nh; ++hh)
+                    if (hh == h) fs = pp.h_fs[hh];
+                Af[mt][ks] = (k < KD && j1 < n1b) ? sT[(fs * KT + j1 + shb0) * LP + l] : 0.0;
+            }
+    } else {
+#pragma unroll
+        for (int ks = 0; ks < KSY; ++ks) {
+            const int r = ks / LQ;
+            const int l = (ks % LQ) * 4 + t4;
+            const bool lv = l < L;
+            Yl[ks] = lv ? l : 0;
+            Yb[ks] = (lv && g8 < n1a) ? sT[(pp.r_code[r] * KT + g8 + sha0) * LP + l] : 0.0;
+            int q = 0;
+#pragma unroll
+            for (int h = 0; h < pp.nh; ++h)
+                if (pp.h_r[h] == r) {
+                    Yc[ks][q] = (lv && g8 < n1b) ? sT[(pp.h_fs[h] * KT + g8 + shb0) * LP + l] : 0.0;
+                    ++q;
+                }
+        }
+    }
+
+    const int i3first = (A == B) ? j3 : 0;
+    for (int i3lo = i3first; i3lo < n3a; i3lo += R3) {
+        const int r3 = cmin(R3, n3a - i3lo);
+        const int ncols = n1a * n2a * r3;
+        __syncthreads();
+        // ---------------- stage A: contract xi3 -> Abar_g[ii3][g][m][l] ----------------
+#pragma unroll
+        for (int g = 0; g < pp.ng; ++g) {
+            for (int it = tid; it < r3 * L * L; it += GEN_THREADS) {
+                const int ii3 = it / (L * L), lm = it - ii3 * (L * L);
+                const int i3 = i3lo + ii3;
+                double acc = 0.0;
+#pragma unroll
+                for (int t = 0; t < pp.nt; ++t) {
+                    if (pp.t_g[t] != g) continue;
+                    const double *Mf = M + pp.t_field[t] * L3 + lm;
+                    const double *Ta = sT + (pp.t_fr[t] * KT + i3 + sha2) * LP;
+                    const double *Tb = sT + (pp.t_fs[t] * KT + j3 + shb2) * LP;
+                    double s = 0.0;
+#pragma unroll
+                    for (int n = 0; n < L; ++n) s = fma(__ldg(Mf + n * L * L), Ta[n] * Tb[n], s);
+                    acc += pp.t_sign[t] > 0 ? s : -s;
+                }
+                const int l = lm / L, m = lm - l * L;
+                sA[((ii3 * NG + g) * L + m) * LP + l] = acc;
+            }
+        }
+        for (int j2lo = 0; j2lo < n2b; j2lo += R2) {
+            const int r2 = cmin(R2, n2b - j2lo);
+            __syncthreads();
+            // ---------------- stage B: contract xi2 -> B_h[jj2][h][ii3][i2][l] ----------------
+#pragma unroll
+            for (int h = 0; h < pp.nh; ++h) {
+                for (int it = tid; it < R2 * R3 * n2a; it += GEN_THREADS) {
+                    const int i2 = it % n2a, q = it / n2a, ii3 = q % R3, jj2 = q / R3;
+                    if (ii3 >= r3 || jj2 >= r2) continue;
+                    const int j2 = j2lo + jj2;
+                    double acc[LP];
+#pragma unroll
+                    for (int l = 0; l < LP; ++l) acc[l] = 0.0;
+#pragma unroll
+                    for (int g = 0; g < pp.ng; ++g) {
+                        if (pp.g_h[g] != h) continue;
+                        const double *Ta = sT + (pp.g_fr[g] * KT + i2 + sha1) * LP;
+                        const double *Tb = sT + (pp.g_fs[g] * KT + j2 + shb1) * LP;
+                        const double *Ag = sA + (ii3 * NG + g) * L * LP;
+#pragma unroll
+                        for (int m = 0; m < L; ++m) {
+                            const double v = Ta[m] * Tb[m];
+                            const double2 *Am = reinterpret_cast<const double2 *>(Ag + m * LP);
+#pragma unroll
+                            for (int l2 = 0; l2 < LP / 2; ++l2) {
+                                const double2 av = Am[l2];
+                                acc[2 * l2] = fma(av.x, v, acc[2 * l2]);
+                                acc[2 * l2 + 1] = fma(av.y, v, acc[2 * l2 + 1]);
+                            }
+                        }
+                    }
+                    double2 *dst = reinterpret_cast<double2 *>(sB + jj2 * SJ2 + ((h * R3 + ii3) * N2 + i2) * LP);
+#pragma unroll
+                    for (int l2 = 0; l2 < LP / 2; ++l2) dst[l2] = make_double2(acc[2 * l2], acc[2 * l2 + 1]);
+                }
+            }
+            __syncthreads();
+            // ---------------- stage C: contract xi1 on DMMA ----------------
+            if constexpr (!YF) {
+                const int nct = (ncols + 7) >> 3;
+                for (int ct = warp; ct < nct; ct += GEN_WARPS) {
+                    const int c = ct * 8 + g8;
+                    const bool cval = c < ncols;
+                    const int i1 = c % n1a, q = c / n1a, i2 = q % n2a, ii3 = q / n2a;
+                    double X[NKS];
+                    int bo[NKS];
+#pragma unroll
+                    for (int ks = 0; ks < NKS; ++ks) {
+                        const int k = ks * 4 + t4;
+                        const int h = k / L, l = k - h * L;
+                        int fr = 0;
+#pragma unroll
+                        for (int hh = 0; hh < pp.nh; ++hh)
+                            if (hh == h) fr = pp.h_fr[hh];
+                        const bool v = k < KD && cval;
+                        X[ks] = v ? sT[(fr * KT + i1 + sha0) * LP + l] : 0.0;
+                        bo[ks] = v ? (h * SH + (ii3 * N2 + i2) * LP + l) : 0;
+                    }
+                    for (int jj2 = 0; jj2 < r2; ++jj2) {
+                        const double *sBj = sB + jj2 * SJ2;
+                        double d[NMT][2];
+#pragma unroll
+                        for (int mt = 0; mt < NMT; ++mt) d[mt][0] = d[mt][1] = 0.0;
+#pragma unroll
+                        for (int ks = 0; ks < NKS; ++ks) {
+                            const double bv = X[ks] * sBj[bo[ks]];
+#pragma unroll
+                            for (int mt = 0; mt < NMT; ++mt) dmma_8x8x4(d[mt][0], d[mt][1], Af[mt][ks], bv);
+                        }
+#pragma unroll
+                        for (int mt = 0; mt < NMT; ++mt) {
+                            const int j1 = mt * 8 + g8;
+                            if (j1 < n1b)
+                                *reinterpret_cast<double2 *>(sS + (jj2 * n1b + j1) * SLD + ct * 8 + 2 * t4) =
+                                    make_double2(d[mt][0], d[mt][1]);
+                        }
+                    }
+                }
+            } else {
+                const int items = R2 * R3 * n2a;
+                for (int it = warp; it < items; it += GEN_WARPS) {
+                    const int i2 = it % n2a, q = it / n2a, ii3 = q % R3, jj2 = q / R3;
+                    if (ii3 >= r3 || jj2 >= r2) continue;
+                    const double *base = sB + jj2 * SJ2 + (ii3 * N2 + i2) * LP;
+                    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < KSY; ++ks) {
+                        const int r = ks / LQ;
+                        double y = 0.0;
+                        int qh = 0;
+#pragma unroll
+                        for (int h = 0; h < pp.nh; ++h)
+                            if (pp.h_r[h] == r) {
+                                y = fma(Yc[ks][qh], base[h * SH + Yl[ks]], y);
+                                ++qh;
+                            }
+                        dmma_8x8x4(d0, d1, y, Yb[ks]);
+                    }
+                    if (g8 < n1b) {
+                        double *dst = sS + (jj2 * n1b + g8) * SLD + (ii3 * n2a + i2) * n1a + 2 * t4;
+                        if (2 * t4 < n1a) dst[0] = d0;
+                        if (2 * t4 + 1 < n1a) dst[1] = d1;
+                    }
+                }
+            }
+            __syncthreads();
+            // ---------------- write-out: contiguous packed row segments ----------------
+            {
+                const int rows = r2 * n1b;
+                const int I0 = offA + n1a * n2a * i3lo;
+                for (int row = warp; row < rows; row += GEN_WARPS) {
+                    const int jj2 = row / n1b, j1 = row - jj2 * n1b;
+                    const int J = offB + j1 + n1b * (j2lo + jj2 + n2b * j3);
+                    const int cs = J > I0 ? J - I0 : 0;
+                    double *rowp = outE + (J * N - J * (J - 1) / 2 - J + I0);
+                    const double *src = sS + row * SLD;
+                    for (int cc = cs + lane; cc < ncols; cc += 32) st_cs(rowp + cc, src[cc]);
+                }
+            }
+        }
+    }
+}
+
+template <int S, int P, int L>
+__global__ void __launch_bounds__(GEN_THREADS, (V2Cfg<S, P, L>::MINB))
+    general_v2_kernel(const __grid_constant__ V2Args args)
+{
+    using C = V2Cfg<S, P, L>;
+    extern __shared__ __align__(16) double smem[];
+    const int u = blockIdx.x % C::NU;
+    const int e = blockIdx.x / C::NU;
+    // decode (b, a, j3): pairs enumerated b-major, a >= b
+    int rem = u, pair = -1, j3 = 0;
+#pragma unroll
+    for (int b = 0; b < C::NB; ++b)
+#pragma unroll
+        for (int a = b; a < C::NB; ++a) {
+            if (pair < 0) {
+                if (rem < C::n(b, 2)) { pair = a * 3 + b; j3 = rem; }
+                else rem -= C::n(b, 2);
+            }
+        }
+    double *sT = smem + C::OFF_T;
+    for (int idx = threadIdx.x; idx < 2 * KT * C::LP; idx += GEN_THREADS) {
+        const int fk = idx / C::LP, l = idx - fk * C::LP;
+        sT[idx] = l < L ? args.tables[TAB_T + fk * LT + l] : 0.0;
+    }
+    __syncthreads();
+    if constexpr (C::NB == 1) {
+        v2_process<S, P, L, 0, 0>(args, smem, e, j3);
+    } else {
+        switch (pair) {
+        case 0: v2_process<S, P, L, 0, 0>(args, smem, e, j3); break;
+        case 3: v2_process<S, P, L, 1, 0>(args, smem, e, j3); break;
+        case 6: v2_process<S, P, L, 2, 0>(args, smem, e, j3); break;
+        case 4: v2_process<S, P, L, 1, 1>(args, smem, e, j3); break;
+        case 7: v2_process<S, P, L, 2, 1>(args, smem, e, j3); break;
+        default: v2_process<S, P, L, 2, 2>(args, smem, e, j3); break;
+        }
+    }
+}
+
+}  // namespace hxg

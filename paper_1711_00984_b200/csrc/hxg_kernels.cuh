@@ -16,12 +16,10 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include "hxg_plan.h"
+#include "hxg_common.cuh"
 
 namespace hxg {
 
-constexpr int GEN_THREADS = 256;
-constexpr int GEN_WARPS = GEN_THREADS / 32;
 constexpr int AFF_THREADS = 128;
 constexpr int MAX_UNITS = 48;  // (block, digit) work units per element: 3 * 13 = 39
 
@@ -285,13 +283,14 @@ __global__ void __launch_bounds__(256) metric_kernel(int space, int L, int E,
          idx += (long long)gridDim.x * blockDim.x) {
         const int e = (int)(idx / L3);
         const int pt = (int)(idx - (long long)e * L3);
-        const int l = pt / (L * L), m = (pt / L) % L, n = pt % L;
+        // metric layout [e][field][n][l][m]: lanes run along m (coalesced stage-A reads)
+        const int n = pt / (L * L), l = (pt / L) % L, m = pt % L;
         const double *par = params + 24LL * e;
         double J[3][3], D[6], C[6], f[MAXF];
         dev_jacobian(kind[e], par, tab[TAB_NODES + l], tab[TAB_NODES + m], tab[TAB_NODES + n], J);
         const double det = dev_metrics(J, D, C);
         const double w = tab[TAB_WTS + l] * tab[TAB_WTS + m] * tab[TAB_WTS + n];
-        const double c = wgrid ? wgrid[(long long)e * L3 + pt] : (coef ? coef[e] : 1.0);
+        const double c = wgrid ? wgrid[(long long)e * L3 + (l * L + m) * L + n] : (coef ? coef[e] : 1.0);
         dev_fields(space, det, D, C, w, c, f);
         double *mo = metric + (long long)e * nfields * L3 + pt;
         for (int k = 0; k < nfields; ++k) mo[(long long)k * L3] = f[k];
@@ -302,13 +301,6 @@ __global__ void __launch_bounds__(256) metric_kernel(int space, int L, int E,
 // ---------------------------------------------------------------------------
 // general map: three-stage sum factorization
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b)
-{
-    asm volatile(
-        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(d0), "+d"(d1)
-        : "d"(a), "d"(b));
-}
 
 // Work unit = (element e, trial block b, trial digit j3): the rows J of the packed
 // output with block b and digit j3, i.e. one contiguous range of packed rows.
@@ -386,11 +378,11 @@ __global__ void __launch_bounds__(GEN_THREADS, (LMAX <= 8 ? 2 : 1))
                     double acc = 0.0;
                     for (int t = 0; t < pp.nt; ++t) {
                         if (pp.t_g[t] != g) continue;
-                        const double *__restrict__ Mf = M + pp.t_field[t] * L3 + (l * L + m) * L;
+                        const double *__restrict__ Mf = M + pp.t_field[t] * L3 + l * L + m;
                         const double *Ta = sT + (pp.t_fr[t] * KT + i3 + sha2) * LP;
                         const double *Tb = sT + (pp.t_fs[t] * KT + j3 + shb2) * LP;
                         double s = 0.0;
-                        for (int n = 0; n < L; ++n) s += __ldg(Mf + n) * (Ta[n] * Tb[n]);
+                        for (int n = 0; n < L; ++n) s += __ldg(Mf + n * L * L) * (Ta[n] * Tb[n]);
                         acc += pp.t_sign[t] > 0 ? s : -s;
                     }
                     sA[((ii3 * NG + g) * L + m) * LP + l] = acc;

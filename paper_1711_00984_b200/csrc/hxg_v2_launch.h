@@ -1,0 +1,12 @@
+// Launchers of the specialized general-map kernels (hxg_gen_*.cu).
+// Each returns 0 on success, 1 if no specialization exists for p, <0 on error.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace hxg {
+struct V2Args;
+int launch_v2_H1(int p, const V2Args &a, cudaStream_t st);
+int launch_v2_hcurl(int p, const V2Args &a, cudaStream_t st);
+int launch_v2_hdiv(int p, const V2Args &a, cudaStream_t st);
+int launch_v2_l2(int p, const V2Args &a, cudaStream_t st);
+}  // namespace hxg
