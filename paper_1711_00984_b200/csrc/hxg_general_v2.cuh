@@ -106,22 +106,40 @@ struct V2Cfg {
     static constexpr int MINB = SMEM_BYTES <= 113 * 1024 ? 2 : 1;
 
     // stage-C factorization per block pair (see file header)
+    __host__ __device__ static constexpr int yq(int a, int b)  // max #h sharing one test function
+    {
+        const CPair pp = make_pair_plan(S, a, b);
+        int q = 1;
+        for (int r = 0; r < pp.nr; ++r) {
+            int hr = 0;
+            for (int h = 0; h < pp.nh; ++h) hr += pp.h_r[h] == r;
+            q = cmax(q, hr);
+        }
+        return q;
+    }
     __host__ __device__ static constexpr bool yform(int a, int b)
     {
         const CPair pp = make_pair_plan(S, a, b);
         if (n(a, 0) > 8 || n(b, 0) > 8) return false;
         const int costB8 = n(a, 0) * ((pp.nh * L + 3) / 4) * 288;
-        int costY = 0;
-        for (int r = 0; r < pp.nr; ++r) {
-            int hr = 0;
-            for (int h = 0; h < pp.nh; ++h) hr += pp.h_r[h] == r;
-            costY += ((L + 3) / 4) * (256 + 32 * hr);
-        }
-        return 8 * costY < costB8;
+        const int costY8 = 8 * ((pp.nr * L + 3) / 4) * (256 + 32 * yq(a, b));
+        return costY8 < costB8;
     }
 };
 
 __device__ __forceinline__ void st_cs(double *p, double v) { __stcs(p, v); }
+
+// bulk (TMA-engine) copy shared -> global, 16-byte aligned, size multiple of 16
+__device__ __forceinline__ void bulk_s2g(double *gdst, const double *ssrc, int bytes)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 template <int S, int P, int L, int A, int B>
 __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int e, int j3)
@@ -150,15 +168,15 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
     constexpr int KD = pp.nh * L;
     constexpr int NKS = (KD + 3) / 4;          // B-form k-steps
     constexpr int NMT = (n1b + 7) / 8;         // B-form row tiles
-    constexpr int LQ = (L + 3) / 4;            // Y-form k-steps per r segment
-    constexpr int KSY = pp.nr * LQ;            // Y-form k-steps
+    constexpr int YQ = C::yq(A, B);            // Y-form trial factors per test function
+    constexpr int KSY = (pp.nr * L + 3) / 4;   // Y-form k-steps (segments may straddle)
     constexpr int NKR = YF ? 1 : NKS;          // register array extents
     constexpr int NYR = YF ? KSY : 1;
     double Af[NMT][NKR];
     double Yb[NYR];
-    double Yc[NYR][2];
-    int Yl[NYR];
-    (void)Af; (void)Yb; (void)Yc; (void)Yl;
+    double Yc[NYR][YQ];
+    int Yo[NYR][YQ];
+    (void)Af; (void)Yb; (void)Yc; (void)Yo;
     if constexpr (!YF) {
 #pragma unroll
         for (int mt = 0; mt < NMT; ++mt)
@@ -173,22 +191,37 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 Af[mt][ks] = (k < KD && j1 < n1b) ? sT[(fs * KT + j1 + shb0) * LP + l] : 0.0;
             }
     } else {
+        // k = r L + l; lane t4 of k-step ks carries k = 4 ks + t4
 #pragma unroll
         for (int ks = 0; ks < KSY; ++ks) {
-            const int r = ks / LQ;
-            const int l = (ks % LQ) * 4 + t4;
-            const bool lv = l < L;
-            Yl[ks] = lv ? l : 0;
-            Yb[ks] = (lv && g8 < n1a) ? sT[(pp.r_code[r] * KT + g8 + sha0) * LP + l] : 0.0;
+            const int k = ks * 4 + t4;
+            const bool kv = k < pp.nr * L;
+            const int r = kv ? k / L : 0, l = kv ? k - (k / L) * L : 0;
+            int rc = 0;
+#pragma unroll
+            for (int rr = 0; rr < pp.nr; ++rr)
+                if (rr == r) rc = pp.r_code[rr];
+            Yb[ks] = (kv && g8 < n1a) ? sT[(rc * KT + g8 + sha0) * LP + l] : 0.0;
+#pragma unroll
+            for (int q = 0; q < YQ; ++q) {
+                Yc[ks][q] = 0.0;
+                Yo[ks][q] = l;
+            }
             int q = 0;
 #pragma unroll
-            for (int h = 0; h < pp.nh; ++h)
-                if (pp.h_r[h] == r) {
-                    Yc[ks][q] = (lv && g8 < n1b) ? sT[(pp.h_fs[h] * KT + g8 + shb0) * LP + l] : 0.0;
-                    ++q;
-                }
+            for (int h = 0; h < pp.nh; ++h) {
+                const bool mine = kv && pp.h_r[h] == r;
+#pragma unroll
+                for (int qq = 0; qq < YQ; ++qq)
+                    if (mine && q == qq) {
+                        Yc[ks][qq] = g8 < n1b ? sT[(pp.h_fs[h] * KT + g8 + shb0) * LP + l] : 0.0;
+                        Yo[ks][qq] = h * SH + l;
+                    }
+                q += mine ? 1 : 0;
+            }
         }
     }
+    const int epar = (int)((reinterpret_cast<size_t>(outE) >> 3) & 1);
 
     const int i3first = (A == B) ? j3 : 0;
     for (int i3lo = i3first; i3lo < n3a; i3lo += R3) {
@@ -253,91 +286,122 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                     for (int l2 = 0; l2 < LP / 2; ++l2) dst[l2] = make_double2(acc[2 * l2], acc[2 * l2 + 1]);
                 }
             }
+            bulk_wait_read();  // previous chunk's bulk stores have read the staging buffer
             __syncthreads();
             // ---------------- stage C: contract xi1 on DMMA ----------------
+            // staging row `row` = (jj2, j1) is shifted by pad(row) in {0,1} doubles so that
+            // it has the 16-byte phase of its global destination (bulk-copy alignment)
+            const int I0 = offA + n1a * n2a * i3lo;
+            auto row_goff = [&](int jj2, int j1) {
+                const int J = offB + j1 + n1b * (j2lo + jj2 + n2b * j3);
+                return J * N - J * (J - 1) / 2 - J + I0;  // &G(J, I0) - outE
+            };
             if constexpr (!YF) {
                 const int nct = (ncols + 7) >> 3;
-                for (int ct = warp; ct < nct; ct += GEN_WARPS) {
-                    const int c = ct * 8 + g8;
-                    const bool cval = c < ncols;
-                    const int i1 = c % n1a, q = c / n1a, i2 = q % n2a, ii3 = q / n2a;
-                    double X[NKS];
-                    int bo[NKS];
-#pragma unroll
-                    for (int ks = 0; ks < NKS; ++ks) {
-                        const int k = ks * 4 + t4;
-                        const int h = k / L, l = k - h * L;
-                        int fr = 0;
-#pragma unroll
-                        for (int hh = 0; hh < pp.nh; ++hh)
-                            if (hh == h) fr = pp.h_fr[hh];
-                        const bool v = k < KD && cval;
-                        X[ks] = v ? sT[(fr * KT + i1 + sha0) * LP + l] : 0.0;
-                        bo[ks] = v ? (h * SH + (ii3 * N2 + i2) * LP + l) : 0;
-                    }
-                    for (int jj2 = 0; jj2 < r2; ++jj2) {
-                        const double *sBj = sB + jj2 * SJ2;
-                        double d[NMT][2];
-#pragma unroll
-                        for (int mt = 0; mt < NMT; ++mt) d[mt][0] = d[mt][1] = 0.0;
+                const int T = nct * r2;
+                const int per = (T + GEN_WARPS - 1) / GEN_WARPS;
+                const int it0 = warp * per, it1 = cmin(T, it0 + per);
+                int ct = -1;
+                double X[NKS];
+                int bo[NKS];
+                for (int it = it0; it < it1; ++it) {
+                    const int ctn = it / r2, jj2 = it - ctn * r2;
+                    if (ctn != ct) {
+                        ct = ctn;
+                        const int c = ct * 8 + g8;
+                        const bool cval = c < ncols;
+                        const int i1 = c % n1a, q = c / n1a, i2 = q % n2a, ii3 = q / n2a;
 #pragma unroll
                         for (int ks = 0; ks < NKS; ++ks) {
-                            const double bv = X[ks] * sBj[bo[ks]];
+                            const int k = ks * 4 + t4;
+                            const int h = k / L, l = k - h * L;
+                            int fr = 0;
 #pragma unroll
-                            for (int mt = 0; mt < NMT; ++mt) dmma_8x8x4(d[mt][0], d[mt][1], Af[mt][ks], bv);
+                            for (int hh = 0; hh < pp.nh; ++hh)
+                                if (hh == h) fr = pp.h_fr[hh];
+                            const bool v = k < KD && cval;
+                            X[ks] = v ? sT[(fr * KT + i1 + sha0) * LP + l] : 0.0;
+                            bo[ks] = v ? (h * SH + (ii3 * N2 + i2) * LP + l) : 0;
                         }
+                    }
+                    const double *sBj = sB + jj2 * SJ2;
+                    double d[NMT][2];
 #pragma unroll
-                        for (int mt = 0; mt < NMT; ++mt) {
-                            const int j1 = mt * 8 + g8;
-                            if (j1 < n1b)
-                                *reinterpret_cast<double2 *>(sS + (jj2 * n1b + j1) * SLD + ct * 8 + 2 * t4) =
-                                    make_double2(d[mt][0], d[mt][1]);
+                    for (int mt = 0; mt < NMT; ++mt) d[mt][0] = d[mt][1] = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < NKS; ++ks) {
+                        const double bv = X[ks] * sBj[bo[ks]];
+#pragma unroll
+                        for (int mt = 0; mt < NMT; ++mt) dmma_8x8x4(d[mt][0], d[mt][1], Af[mt][ks], bv);
+                    }
+#pragma unroll
+                    for (int mt = 0; mt < NMT; ++mt) {
+                        const int j1 = mt * 8 + g8;
+                        if (j1 < n1b) {
+                            const int pad = (epar + row_goff(jj2, j1)) & 1;
+                            double *dst = sS + (jj2 * n1b + j1) * SLD + pad + ct * 8 + 2 * t4;
+                            dst[0] = d[mt][0];
+                            dst[1] = d[mt][1];
                         }
                     }
                 }
             } else {
-                const int items = R2 * R3 * n2a;
-                for (int it = warp; it < items; it += GEN_WARPS) {
-                    const int i2 = it % n2a, q = it / n2a, ii3 = q % R3, jj2 = q / R3;
-                    if (ii3 >= r3 || jj2 >= r2) continue;
+                const int T = r3 * n2a * r2;  // tiles (ii3, i2, jj2), jj2 fastest
+                const int per = (T + GEN_WARPS - 1) / GEN_WARPS;
+                const int it0 = warp * per, it1 = cmin(T, it0 + per);
+                int qd = it0 / r2, jj2 = it0 - qd * r2;
+                int ii3 = qd / n2a, i2 = qd - ii3 * n2a;
+                for (int it = it0; it < it1; ++it) {
                     const double *base = sB + jj2 * SJ2 + (ii3 * N2 + i2) * LP;
                     double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                     for (int ks = 0; ks < KSY; ++ks) {
-                        const int r = ks / LQ;
-                        double y = 0.0;
-                        int qh = 0;
+                        double y = Yc[ks][0] * base[Yo[ks][0]];
 #pragma unroll
-                        for (int h = 0; h < pp.nh; ++h)
-                            if (pp.h_r[h] == r) {
-                                y = fma(Yc[ks][qh], base[h * SH + Yl[ks]], y);
-                                ++qh;
-                            }
+                        for (int q = 1; q < YQ; ++q) y = fma(Yc[ks][q], base[Yo[ks][q]], y);
                         dmma_8x8x4(d0, d1, y, Yb[ks]);
                     }
                     if (g8 < n1b) {
-                        double *dst = sS + (jj2 * n1b + g8) * SLD + (ii3 * n2a + i2) * n1a + 2 * t4;
+                        const int pad = (epar + row_goff(jj2, g8)) & 1;
+                        double *dst = sS + (jj2 * n1b + g8) * SLD + pad + (ii3 * n2a + i2) * n1a + 2 * t4;
                         if (2 * t4 < n1a) dst[0] = d0;
                         if (2 * t4 + 1 < n1a) dst[1] = d1;
                     }
+                    if (++jj2 == r2) {
+                        jj2 = 0;
+                        if (++i2 == n2a) { i2 = 0; ++ii3; }
+                    }
                 }
             }
+            fence_proxy_async();  // staging writes -> visible to the bulk-copy (async) proxy
             __syncthreads();
-            // ---------------- write-out: contiguous packed row segments ----------------
+            // ---------------- write-out: one bulk copy per packed row segment ----------------
             {
                 const int rows = r2 * n1b;
-                const int I0 = offA + n1a * n2a * i3lo;
-                for (int row = warp; row < rows; row += GEN_WARPS) {
+                for (int row = tid; row < rows; row += GEN_THREADS) {
                     const int jj2 = row / n1b, j1 = row - jj2 * n1b;
+                    const int goff = row_goff(jj2, j1);
                     const int J = offB + j1 + n1b * (j2lo + jj2 + n2b * j3);
-                    const int cs = J > I0 ? J - I0 : 0;
-                    double *rowp = outE + (J * N - J * (J - 1) / 2 - J + I0);
-                    const double *src = sS + row * SLD;
-                    for (int cc = cs + lane; cc < ncols; cc += 32) st_cs(rowp + cc, src[cc]);
+                    int cs = J > I0 ? J - I0 : 0;
+                    if (cs >= ncols) continue;
+                    const int pad = (epar + goff) & 1;
+                    const double *src = sS + row * SLD + pad + cs;
+                    double *dst = outE + goff + cs;
+                    int len = ncols - cs;
+                    if (reinterpret_cast<size_t>(dst) & 8) {  // 8-byte head
+                        st_cs(dst, *src);
+                        ++dst;
+                        ++src;
+                        --len;
+                    }
+                    if (len & 1) st_cs(dst + len - 1, src[len - 1]);  // 8-byte tail
+                    if (len >= 2) bulk_s2g(dst, src, (len & ~1) * 8);
                 }
+                bulk_commit();
             }
         }
     }
+    bulk_wait_all();
 }
 
 template <int S, int P, int L>
