@@ -1,5 +1,7 @@
+#include <cstdlib>
 // Specialized general-map kernels for space H1, isotropic orders p = 1..10, L = p + 1.
 #include "hxg_general_v2.cuh"
+#include "hxg_general_v3.cuh"
 #include "hxg_v2_launch.h"
 
 namespace hxg {
@@ -7,6 +9,29 @@ namespace hxg {
 template <int P>
 static int launch_one(const V2Args &a, int grid, cudaStream_t st)
 {
+    using C3 = V3Cfg<H1, P, P + 1>;
+    // general_v3_kernel<H1, 7, 8> is miscompiled by ptxas -O3 (CUDA 12.9; wrong
+    // results that change with unrelated dead code, correct at -Xptxas -O0;
+    // repro: tools/dbg_v3.cu) -- p = 7 runs the CTA-chunked v2 kernel instead.
+    if constexpr (C3::OK && P != 7) {
+        if (!(getenv("HXG_FORCE_V2") && getenv("HXG_FORCE_V2")[0] == '1')) {
+            auto k3 = general_v3_kernel<H1, P, P + 1>;
+            if (cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM_BYTES) != cudaSuccess)
+                return -5;
+            V3Args b;
+            b.tables = a.tables;
+            b.metric = a.metric;
+            b.out = a.out;
+            b.P = a.P;
+            b.E = a.E;
+            const int want = 148 * C3::MINB * 2;
+            b.split = a.E >= want ? 1 : (want + a.E - 1) / a.E;
+            if (b.split > 16) b.split = 16;
+            if (getenv("HXG_V3_SPLIT")) b.split = atoi(getenv("HXG_V3_SPLIT"));
+            k3<<<a.E * b.split, V3_THREADS, C3::SMEM_BYTES, st>>>(b);
+            return cudaGetLastError() == cudaSuccess ? 0 : -5;
+        }
+    }
     using C = V2Cfg<H1, P, P + 1>;
     auto k = general_v2_kernel<H1, P, P + 1>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)

@@ -1,0 +1,426 @@
+// hxg_general_v3.cuh -- warp-per-work-unit general-map Gram kernel
+// (compile-time space / order / rule; orders with every digit extent <= 8 and
+// L <= 8, i.e. the BASELINE configs 1-4).
+//
+// Each warp owns one work unit at a time -- (element e, trial block b, test
+// block a >= b, digits j3, i3) -- and runs all three sum-factorization stages
+// for it with warp-private shared memory, so no CTA-wide barrier ever stalls
+// the FP64 pipe:
+//   stage A (xi3, DFMA)   Abar_g[m][l] = sum_t sign_t sum_n M_t[n][l,m] u(i3,n) u(j3,n)
+//   for every trial digit j2:
+//     stage B (xi2, DMMA) B_h[i2][l] = sum_{g in h} sum_m V_g[i2][m] Abar_g[m][l]
+//     stage C (xi1, DMMA) Y-form or B-form (see hxg_general_v2.cuh), one 8x8
+//                         tile per test digit i2 (Y) or i1 (B)
+//     write-out           one bulk copy (cp.async.bulk, TMA engine) per packed
+//                         row segment, double-buffered staging
+// CTAs of 4 warps take the work units of one element from a shared-memory
+// counter (dynamic balancing; the element's metric stays L1/L2-resident).
+#pragma once
+#include "hxg_common.cuh"
+#include "hxg_general_v2.cuh"
+#include "hxg_terms.h"
+
+namespace hxg {
+
+#ifndef HXG_V3_DEBUG_EMIN
+#define HXG_V3_DEBUG_EMIN 0
+#endif
+#ifndef HXG_V3_I2_UNROLL
+#define HXG_V3_I2_UNROLL 8
+#endif
+constexpr int kI2Unroll = HXG_V3_I2_UNROLL;
+#if defined(HXG_V3_DEBUG) || defined(HXG_V3_DEBUG2)
+__device__ double *hxg_dbg;
+#endif
+constexpr int V3_WARPS = 4;
+constexpr int V3_THREADS = V3_WARPS * 32;
+
+template <int S, int P, int L>
+struct V3Cfg {
+    using C2 = V2Cfg<S, P, L>;
+    static constexpr int NB = C2::NB, NF = C2::NF, L3 = C2::L3, N = C2::N;
+    static constexpr int NG = C2::NG, NH = C2::NH, C12 = C2::C12;
+    __host__ __device__ static constexpr int n(int a, int d) { return C2::n(a, d); }
+    static constexpr bool OK = L <= 8 && C2::N1 <= 8 && C2::N2 <= 8;
+    __host__ __device__ static constexpr int maxt()
+    {
+        int m = 1;
+        for (int a = 0; a < NB; ++a)
+            for (int b = 0; b < NB; ++b) m = cmax(m, make_pair_plan(S, a, b).nt);
+        return m;
+    }
+    static constexpr int NT = maxt();
+    static constexpr int LP = (L + 1) & ~1;      // sT row stride
+    static constexpr int SW = ((C12 + 1 + 1) / 2) * 2;  // staging row stride (even, >= C12 + 1)
+    // per-warp shared memory (doubles)
+    static constexpr int W_P = 0;                       // [NT][8]   stage-A 1D products
+    static constexpr int W_A = W_P + NT * 8;            // [NG][8][8] Abar (rows m, cols l; zero padded)
+    static constexpr int W_B = W_A + NG * 64;           // [NH][8][8] B_h (rows i2, cols l)
+    static constexpr int W_S = W_B + NH * 64;           // [2][8][SW] staging
+    static constexpr int W_TOT = W_S + 2 * 8 * SW;
+    static constexpr int OFF_T = 0;                     // CTA-shared [2][KT][LP]
+    static constexpr int OFF_W = 2 * KT * LP;
+    static constexpr int SMEM_BYTES = (OFF_W + V3_WARPS * W_TOT) * 8 + 16;
+    __host__ __device__ static constexpr int pair_units(int a, int b)
+    {
+        return a == b ? n(a, 2) * (n(a, 2) + 1) / 2 : n(a, 2) * n(b, 2);
+    }
+    __host__ __device__ static constexpr int units()
+    {
+        int u = 0;
+        for (int b = 0; b < NB; ++b)
+            for (int a = b; a < NB; ++a) u += pair_units(a, b);
+        return u;
+    }
+    static constexpr int NU = units();
+#ifdef HXG_V3_MINB
+    static constexpr int MINB = HXG_V3_MINB;
+#else
+    static constexpr int MINB = cmin(8, (228 * 1024) / (SMEM_BYTES + 1024));
+#endif
+};
+
+struct V3Args {
+    const double *tables;
+    const double *metric;  // [E][nfields][n][l][m]
+    double *out;
+    long long P;
+    int E;
+    int split;  // CTAs per element
+};
+
+// explicit shared-memory load (ordered after the warp barrier that publishes B_h)
+__device__ __forceinline__ double lds_f64(const double *p)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+
+template <int S, int P, int L, int A, int B>
+__device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, double *W,
+                                        const double *__restrict__ M, double *__restrict__ outE,
+                                        int epar, int j3, int i3, int &buf, unsigned &keep)
+{
+    using C = V3Cfg<S, P, L>;
+    constexpr CPair pp = make_pair_plan(S, A, B);
+    constexpr int LP = C::LP, L3 = C::L3, N = C::N, SW = C::SW;
+    constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1);
+    constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1);
+    constexpr int sha0 = sh_of(S, A, 0), sha1 = sh_of(S, A, 1), sha2 = sh_of(S, A, 2);
+    constexpr int shb0 = sh_of(S, B, 0), shb1 = sh_of(S, B, 1), shb2 = sh_of(S, B, 2);
+    constexpr int offA = V2Cfg<S, P, L>::off(A), offB = V2Cfg<S, P, L>::off(B);
+    constexpr bool YF = V2Cfg<S, P, L>::yform(A, B);
+    constexpr int LQ = (L + 3) / 4;  // k-steps over a length-L contraction
+    constexpr int ncols = n1a * n2a;
+    const int lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
+    double *sP = W + C::W_P, *sA = W + C::W_A, *sBw = W + C::W_B;
+
+    // ---------------- stage A: contract xi3 ----------------
+    for (int o = lane; o < pp.nt * 8; o += 32) {
+        const int t = o >> 3, n = o & 7;
+        int fr = 0, fs = 0;
+#pragma unroll
+        for (int tt = 0; tt < pp.nt; ++tt)
+            if (tt == t) { fr = pp.t_fr[tt]; fs = pp.t_fs[tt]; }
+        sP[o] = n < L ? sT[(fr * KT + i3 + sha2) * LP + n] * sT[(fs * KT + j3 + shb2) * LP + n] : 0.0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g = 0; g < pp.ng; ++g) {
+#pragma unroll
+        for (int lm0 = 0; lm0 < L * L; lm0 += 32) {
+            const int lm = lm0 + lane;
+            if (lm < L * L) {
+                double acc = 0.0;
+#pragma unroll
+                for (int t = 0; t < pp.nt; ++t) {
+                    if (pp.t_g[t] != g) continue;
+                    const double *Mf = M + pp.t_field[t] * L3 + lm;
+                    const double *pt = sP + t * 8;
+                    double s = 0.0;
+#pragma unroll
+                    for (int n = 0; n < L; ++n) s = fma(__ldg(Mf + n * L * L), pt[n], s);
+                    acc += pp.t_sign[t] > 0 ? s : -s;
+                }
+                const int l = lm / L, m = lm - l * L;
+                sA[(g * 8 + m) * 8 + l] = acc;
+            }
+        }
+    }
+    __syncwarp();
+
+    // ---------------- per-unit operand registers ----------------
+    // stage B: A operand V_g[i2 = g8][m] = u_{fr}(i2, m) * u_{fs}(j2, m); Ta = test factor
+    double Ta[2][LQ];
+#pragma unroll
+    for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+        for (int ks = 0; ks < LQ; ++ks) {
+            const int m = ks * 4 + t4;
+            Ta[fr][ks] = (m < L && g8 < n2a) ? sT[(fr * KT + g8 + sha1) * LP + m] : 0.0;
+        }
+    // stage C operands
+    constexpr int KD = pp.nh * L, NKS = (KD + 3) / 4;
+    constexpr int YQ = V2Cfg<S, P, L>::yq(A, B);
+    constexpr int KSY = (pp.nr * L + 3) / 4;
+    constexpr int NR1 = YF ? KSY : NKS;
+    double R0[NR1];   // Y: Yb (u_r(i1 = g8, l))   B: Af (u_s(j1 = g8, l))
+    double Yc[YF ? KSY : 1][YQ];
+    int Ro[NR1][YF ? YQ : 1];  // Y: sBw offsets per factor   B: sBw offset (h, i2 = g8, l)
+    int Xo[YF ? 1 : NKS];      // B: sT offset of u_r(0 + sha0, l) for the test factor
+    (void)Yc;
+    (void)Xo;
+    if constexpr (YF) {
+#pragma unroll
+        for (int ks = 0; ks < KSY; ++ks) {
+            const int k = ks * 4 + t4;
+            const bool kv = k < pp.nr * L;
+            const int r = kv ? k / L : 0, l = kv ? k - r * L : 0;
+            int rc = 0;
+#pragma unroll
+            for (int rr = 0; rr < pp.nr; ++rr)
+                if (rr == r) rc = pp.r_code[rr];
+            R0[ks] = (kv && g8 < n1a) ? sT[(rc * KT + g8 + sha0) * LP + l] : 0.0;
+#pragma unroll
+            for (int q = 0; q < YQ; ++q) {
+                Yc[ks][q] = 0.0;
+                Ro[ks][q] = l;
+            }
+            int q = 0;
+#pragma unroll
+            for (int h = 0; h < pp.nh; ++h) {
+                const bool mine = kv && pp.h_r[h] == r;
+#pragma unroll
+                for (int qq = 0; qq < YQ; ++qq)
+                    if (mine && q == qq) {
+                        Yc[ks][qq] = g8 < n1b ? sT[(pp.h_fs[h] * KT + g8 + shb0) * LP + l] : 0.0;
+                        Ro[ks][qq] = h * 64 + l;
+                    }
+                q += mine ? 1 : 0;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int ks = 0; ks < NKS; ++ks) {
+            const int k = ks * 4 + t4;
+            const bool kv = k < KD;
+            const int h = kv ? k / L : 0, l = kv ? k - h * L : 0;
+            int fs = 0, fr = 0;
+#pragma unroll
+            for (int hh = 0; hh < pp.nh; ++hh)
+                if (hh == h) { fs = pp.h_fs[hh]; fr = pp.h_fr[hh]; }
+            R0[ks] = (kv && g8 < n1b) ? sT[(fs * KT + g8 + shb0) * LP + l] : 0.0;
+            Ro[ks][0] = h * 64 + g8 * 8 + l;
+            Xo[ks] = kv ? (fr * KT + sha0) * LP + l : 0;  // invalid k: A operand is 0
+        }
+    }
+
+    const int I0 = offA + ncols * i3;
+    for (int j2 = 0; j2 < n2b; ++j2) {
+        // ---------------- stage B: contract xi2 on DMMA ----------------
+        double Tb[2][LQ];
+#pragma unroll
+        for (int fs = 0; fs < 2; ++fs)
+#pragma unroll
+            for (int ks = 0; ks < LQ; ++ks) {
+                const int m = ks * 4 + t4;
+                Tb[fs][ks] = m < L ? sT[(fs * KT + j2 + shb1) * LP + m] : 0.0;
+            }
+#pragma unroll
+        for (int h = 0; h < pp.nh; ++h) {
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int g = 0; g < pp.ng; ++g) {
+                if (pp.g_h[g] != h) continue;
+#pragma unroll
+                for (int ks = 0; ks < LQ; ++ks) {
+                    const double av = Ta[pp.g_fr[g]][ks] * Tb[pp.g_fs[g]][ks];
+                    const double bv = sA[(g * 8 + ks * 4 + t4) * 8 + g8];
+                    dmma_8x8x4_keep(d0, d1, av, bv, keep);
+                }
+            }
+            sBw[(h * 8 + g8) * 8 + 2 * t4] = d0;
+            sBw[(h * 8 + g8) * 8 + 2 * t4 + 1] = d1;
+        }
+        __syncwarp();
+        // staging buffer `buf` was last read by the bulk copies issued two rows-groups ago
+        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        __syncwarp();
+
+        double *sS = W + C::W_S + buf * 8 * SW;
+        const int J = offB + g8 + n1b * (j2 + n2b * j3);  // row of this lane's j1 = g8
+        const int goff = J * N - J * (J - 1) / 2 - J + I0;
+        const int pad = (epar + goff) & 1;
+        double *srow = sS + g8 * SW + pad;
+        // ---------------- stage C: contract xi1 on DMMA ----------------
+        if constexpr (YF) {
+#pragma unroll kI2Unroll
+            for (int i2 = 0; i2 < n2a; ++i2) {
+                const double *base = sBw + i2 * 8;
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KSY; ++ks) {
+                    double y = Yc[ks][0] * base[Ro[ks][0]];
+#pragma unroll
+                    for (int q = 1; q < YQ; ++q) y = fma(Yc[ks][q], base[Ro[ks][q]], y);
+                    dmma_8x8x4_keep(d0, d1, y, R0[ks], keep);
+                }
+                if (g8 < n1b) {
+                    if (2 * t4 < n1a) srow[i2 * n1a + 2 * t4] = d0;
+                    if (2 * t4 + 1 < n1a) srow[i2 * n1a + 2 * t4 + 1] = d1;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i1 = 0; i1 < n1a; ++i1) {
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < NKS; ++ks) {
+                    const double bv = sT[Xo[ks] + i1 * LP] * sBw[Ro[ks][0]];
+                    dmma_8x8x4_keep(d0, d1, R0[ks], bv, keep);
+                }
+                if (g8 < n1b) {  // columns i2 = 2 t4, 2 t4 + 1
+                    if (2 * t4 < n2a) srow[(2 * t4) * n1a + i1] = d0;
+                    if (2 * t4 + 1 < n2a) srow[(2 * t4 + 1) * n1a + i1] = d1;
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        // ---------------- write-out: lane j1 copies packed row J from column max(J, I0) ----------------
+#ifdef HXG_V3_SIMPLE_WO
+        for (int j1 = 0; j1 < n1b; ++j1) {
+            const int Jr = offB + j1 + n1b * (j2 + n2b * j3);
+            const int goffr = Jr * N - Jr * (Jr - 1) / 2 - Jr + I0;
+            const int padr = (epar + goffr) & 1;
+            const int csr = Jr > I0 ? Jr - I0 : 0;
+            const double *srcr = sS + j1 * SW + padr;
+            for (int c = csr + lane; c < ncols; c += 32) outE[goffr + c] = srcr[c];
+        }
+        if (false) {
+#else
+        if (g8 < n1b && t4 == 0) {
+#endif
+            const int cs = J > I0 ? J - I0 : 0;
+            if (cs < ncols) {
+                const double *src = srow + cs;
+                double *dst = outE + goff + cs;
+                int len = ncols - cs;
+                if (reinterpret_cast<size_t>(dst) & 8) {
+                    __stcs(dst, *src);
+                    ++dst;
+                    ++src;
+                    --len;
+                }
+                if (len & 1) __stcs(dst + len - 1, src[len - 1]);
+#ifdef HXG_V3_NO_BULK
+                for (int c = 0; c < (len & ~1); ++c) __stcs(dst + c, src[c]);
+#else
+                if (len >= 2) bulk_s2g(dst, src, (len & ~1) * 8);
+#endif
+            }
+        }
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        buf ^= 1;
+        __syncwarp();  // reconverge after the divergent write-out: the next mma.sync needs the full warp
+    }
+#ifdef HXG_V3_DEBUG2
+    if (blockIdx.x == 0 && j3 == 0 && i3 == 0 && args.E > HXG_V3_DEBUG_EMIN) {
+#if HXG_V3_DEBUG2 & 1
+        for (int q = lane; q < C::NG * 64; q += 32) hxg_dbg[q] = sA[q];
+        for (int q = lane; q < C::NH * 64; q += 32) hxg_dbg[1024 + q] = sBw[q];
+#endif
+#if HXG_V3_DEBUG2 & 2
+        if constexpr (YF) {
+            for (int ks = 0; ks < KSY; ++ks) {
+                hxg_dbg[2048 + ks * 32 + lane] = R0[ks];
+                hxg_dbg[2304 + ks * 32 + lane] = Yc[ks][0];
+                hxg_dbg[2560 + ks * 32 + lane] = Yc[ks][YQ - 1];
+                hxg_dbg[2816 + ks * 32 + lane] = Ro[ks][0];
+                hxg_dbg[3072 + ks * 32 + lane] = Ro[ks][YQ - 1];
+            }
+        }
+#endif
+#if HXG_V3_DEBUG2 & 4
+        const double *sSl = W + C::W_S + (buf ^ 1) * 8 * SW;
+        for (int q = lane; q < 8 * SW; q += 32) hxg_dbg[3328 + q] = sSl[q];
+#endif
+    }
+#endif
+}
+
+template <int S, int P, int L>
+__global__ void __launch_bounds__(V3_THREADS, (V3Cfg<S, P, L>::MINB))
+    general_v3_kernel(const __grid_constant__ V3Args args)
+{
+    using C = V3Cfg<S, P, L>;
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_next;
+    const int e = blockIdx.x / args.split;
+    const int part = blockIdx.x - e * args.split;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *sT = smem + C::OFF_T;
+    for (int idx = threadIdx.x; idx < 2 * KT * C::LP; idx += V3_THREADS) {
+        const int fk = idx / C::LP, l = idx - fk * C::LP;
+        sT[idx] = l < L ? args.tables[TAB_T + fk * LT + l] : 0.0;
+    }
+    double *W = smem + C::OFF_W + warp * C::W_TOT;
+    for (int idx = lane; idx < C::W_TOT; idx += 32) W[idx] = 0.0;  // zero padding of Abar/B_h
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+    const double *__restrict__ M = args.metric + (long long)e * C::NF * C::L3;
+    double *__restrict__ outE = args.out + (long long)e * args.P;
+    const int epar = (int)((reinterpret_cast<size_t>(outE) >> 3) & 1);
+    const int lo = (int)((long long)C::NU * part / args.split);
+    const int hi = (int)((long long)C::NU * (part + 1) / args.split);
+    int buf = 0;
+    unsigned keep = 0;  // see dmma_8x8x4_keep
+    for (;;) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(&s_next, 1);
+        u = __shfl_sync(0xffffffffu, u, 0) + lo;
+        if (u >= hi) break;
+        // decode (b, a) pair, then (j3, i3)
+        int rem = u, pair = -1, j3 = 0, i3 = 0;
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b)
+#pragma unroll
+            for (int a = b; a < C::NB; ++a) {
+                if (pair < 0) {
+                    const int cnt = C::pair_units(a, b);
+                    if (rem < cnt) {
+                        pair = a * 3 + b;
+                        if (a == b) {  // j3 <= i3 < n3
+                            const int n3 = C::n(a, 2);
+                            int jj = 0, r = rem;
+                            while (r >= n3 - jj) { r -= n3 - jj; ++jj; }
+                            j3 = jj;
+                            i3 = jj + r;
+                        } else {
+                            j3 = rem / C::n(a, 2);
+                            i3 = rem - j3 * C::n(a, 2);
+                        }
+                    } else {
+                        rem -= cnt;
+                    }
+                }
+            }
+        if constexpr (C::NB == 1) {
+            v3_unit<S, P, L, 0, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep);
+        } else {
+            switch (pair) {
+            case 0: v3_unit<S, P, L, 0, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 3: v3_unit<S, P, L, 1, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 6: v3_unit<S, P, L, 2, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 4: v3_unit<S, P, L, 1, 1>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 7: v3_unit<S, P, L, 2, 1>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            default: v3_unit<S, P, L, 2, 2>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            }
+        }
+    }
+    if (args.E < 0 && keep == 0x9e3779b9u) args.out[0] = keep;  // never taken; keeps `keep` live
+    bulk_wait_all();
+}
+
+}  // namespace hxg
