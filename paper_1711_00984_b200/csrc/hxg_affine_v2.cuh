@@ -1,0 +1,243 @@
+// hxg_affine_v2.cuh -- compile-time specialized constant-Jacobian (affine) Gram
+// kernel: simp_*_const of the reference (_kernels.py:1169-1404).
+//
+// With constant J every 1D integral is a closed-form F-table entry, so
+//   G[J, I] = sum_h F_h[i1 + sa][j1 + sb] * Bs_h[a, i2, i3]     (<= 4 FMAs per entry)
+//   Bs_h    = sum_{g in h} F_g[i2][j2] * sum_{t in g} sign * field_t * F_t[i3][j3]
+// and the kernel is bound by the packed-output write.  One CTA owns the n1b
+// packed rows J = (j1, j2, j3, b); threads (j1, i1, K-slot) evaluate one entry
+// per column group K = (i2, i3) into a shared-memory row image, which is sent
+// to HBM with one bulk copy (cp.async.bulk) per row and test block.
+#pragma once
+#include "hxg_common.cuh"
+#include "hxg_general_v2.cuh"
+#include "hxg_geom.cuh"
+#include "hxg_terms.h"
+
+namespace hxg {
+
+constexpr int AFF2_THREADS = 128;
+
+struct AffV2Args {
+    const int *kind;
+    const double *params, *coef, *tables;
+    double *out;
+    int *status;
+    long long P;
+    int E;
+};
+
+template <int S, int P>
+struct AffCfg {
+    static constexpr int NB = nb_of(S);
+    __host__ __device__ static constexpr int n(int a, int d) { return ext_of(S, P, a, d); }
+    __host__ __device__ static constexpr int blk(int a) { return n(a, 0) * n(a, 1) * n(a, 2); }
+    __host__ __device__ static constexpr int off(int a)
+    {
+        return a == 0 ? 0 : (a == 1 ? blk(0) : blk(0) + blk(1));
+    }
+    static constexpr int N = off(NB - 1) + blk(NB - 1);
+    __host__ __device__ static constexpr int nmax(int d)
+    {
+        return cmax(n(0, d), NB > 1 ? cmax(n(1, d), n(2, d)) : 0);
+    }
+    static constexpr int N1 = nmax(0);
+    static constexpr int NK = cmax(n(0, 1) * n(0, 2), NB > 1 ? cmax(n(1, 1) * n(1, 2), n(2, 1) * n(2, 2)) : 0);
+    static constexpr int BMAX = cmax(blk(0), NB > 1 ? cmax(blk(1), blk(2)) : 0);
+    static constexpr int KF = P + 2;                 // F-table index range needed
+    static constexpr int SWA = ((BMAX + 2) / 2) * 2;  // staging row stride (>= BMAX + 1, even)
+    static constexpr int OFF_F = 0;                  // [4][KF][KF]
+    static constexpr int OFF_B = OFF_F + 4 * KF * KF;  // [NB][NK][4]
+    static constexpr int OFF_S = ((OFF_B + NB * NK * 4 + 1) / 2) * 2;  // [2][N1][SWA]
+    static constexpr int SMEM_BYTES = (OFF_S + 2 * N1 * SWA) * 8;
+    __host__ __device__ static constexpr int units()
+    {
+        int u = 0;
+        for (int b = 0; b < NB; ++b) u += n(b, 1) * n(b, 2);
+        return u;
+    }
+    static constexpr int NU = units();
+};
+
+template <int S, int P, int A, int B>
+__device__ __forceinline__ void aff_block(double *smem, double *__restrict__ outE, int epar, int j2,
+                                          int j3, int &buf)
+{
+    using C = AffCfg<S, P>;
+    constexpr CPair pp = make_pair_plan(S, A, B);
+    constexpr int KF = C::KF, SWA = C::SWA, N = C::N;
+    constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1), n3a = C::n(A, 2);
+    constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1);
+    constexpr int sha0 = sh_of(S, A, 0), shb0 = sh_of(S, B, 0);
+    constexpr int offA = C::off(A), offB = C::off(B);
+    constexpr int TPK = n1a * n1b;                       // threads per column group
+    constexpr int KS = AFF2_THREADS / TPK;               // column groups in flight
+    const double *sF = smem + C::OFF_F;
+    const double *sBs = smem + C::OFF_B + A * C::NK * 4;
+    double *sS = smem + C::OFF_S + buf * C::N1 * SWA;
+    const int tid = threadIdx.x;
+
+    const int Kp = j2 + n2b * j3;                        // trial column group
+    const int K0 = (A == B) ? Kp : 0;                    // first needed test group
+    const int nK = n2a * n3a - K0;
+    const int I0 = offA + K0 * n1a;                      // first column of the image
+
+    // this thread's (j1, i1) and its F factors
+    const int slot = tid / TPK, r = tid - slot * TPK;
+    const int j1 = r / n1a, i1 = r - j1 * n1a;
+    double Fr[MAXH];
+#pragma unroll
+    for (int h = 0; h < MAXH; ++h)
+        Fr[h] = (h < pp.nh && slot < KS)
+                    ? sF[((2 * pp.h_fr[h] + pp.h_fs[h]) * KF + i1 + sha0) * KF + j1 + shb0]
+                    : 0.0;
+    if (slot < KS) {
+        const int J = offB + j1 + n1b * Kp;
+        const int goff = J * N - J * (J - 1) / 2 - J + I0;
+        const int pad = (epar + goff) & 1;
+        double *srow = sS + j1 * SWA + pad + i1;
+        for (int k = slot; k < nK; k += KS) {
+            const double2 b01 = *reinterpret_cast<const double2 *>(sBs + (K0 + k) * 4);
+            double v = Fr[0] * b01.x;
+            if (pp.nh > 1) v = fma(Fr[1], b01.y, v);
+            if (pp.nh > 2) {
+                const double2 b23 = *reinterpret_cast<const double2 *>(sBs + (K0 + k) * 4 + 2);
+                v = fma(Fr[2], b23.x, v);
+                if (pp.nh > 3) v = fma(Fr[3], b23.y, v);
+            }
+            srow[k * n1a] = v;
+        }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid < n1b) {
+        const int J = offB + tid + n1b * Kp;
+        const int goff = J * N - J * (J - 1) / 2 - J + I0;
+        const int pad = (epar + goff) & 1;
+        const int ncols = nK * n1a;
+        const int cs = J > I0 ? J - I0 : 0;
+        if (cs < ncols) {
+            const double *src = sS + tid * SWA + pad + cs;
+            double *dst = outE + goff + cs;
+            int len = ncols - cs;
+            if (reinterpret_cast<size_t>(dst) & 8) {
+                __stcs(dst, *src);
+                ++dst;
+                ++src;
+                --len;
+            }
+            if (len & 1) __stcs(dst + len - 1, src[len - 1]);
+            if (len >= 2) bulk_s2g(dst, src, (len & ~1) * 8);
+        }
+        bulk_commit();
+        // the other staging buffer is rewritten by the next block: its copies must have read it
+        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+    }
+    __syncthreads();
+    buf ^= 1;
+}
+
+// Bs_h[A][K] for one (test block A, trial block B) pair
+template <int S, int P, int A, int B>
+__device__ __forceinline__ void aff_bsum(double *smem, const double *s_field, int j2, int j3)
+{
+    using C = AffCfg<S, P>;
+    constexpr CPair pp = make_pair_plan(S, A, B);
+    constexpr int KF = C::KF, n2a = C::n(A, 1), n3a = C::n(A, 2);
+    constexpr int sa1 = sh_of(S, A, 1), sa2 = sh_of(S, A, 2), sb1 = sh_of(S, B, 1), sb2 = sh_of(S, B, 2);
+    const double *sF = smem + C::OFF_F;
+    for (int k = threadIdx.x; k < n2a * n3a; k += AFF2_THREADS) {
+        const int i2 = k % n2a, i3 = k / n2a;
+        double acc[MAXH] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int g = 0; g < pp.ng; ++g) {
+            double sg = 0.0;
+#pragma unroll
+            for (int t = 0; t < pp.nt; ++t) {
+                if (pp.t_g[t] != g) continue;
+                const double f = sF[((2 * pp.t_fr[t] + pp.t_fs[t]) * KF + i3 + sa2) * KF + j3 + sb2];
+                const double v = s_field[pp.t_field[t]] * f;
+                sg += pp.t_sign[t] > 0 ? v : -v;
+            }
+            const double fb = sF[((2 * pp.g_fr[g] + pp.g_fs[g]) * KF + i2 + sa1) * KF + j2 + sb1];
+            acc[pp.g_h[g]] = fma(fb, sg, acc[pp.g_h[g]]);
+        }
+        double2 *dst = reinterpret_cast<double2 *>(smem + C::OFF_B + (A * C::NK + k) * 4);
+        dst[0] = make_double2(acc[0], acc[1]);
+        dst[1] = make_double2(acc[2], acc[3]);
+    }
+}
+
+template <int S, int P>
+__global__ void __launch_bounds__(AFF2_THREADS) affine_v2_kernel(const __grid_constant__ AffV2Args args)
+{
+    using C = AffCfg<S, P>;
+    constexpr int KF = C::KF;
+    extern __shared__ __align__(16) double smem[];
+    __shared__ double s_field[MAXF];
+    const int tid = threadIdx.x;
+    const int u = blockIdx.x % C::NU;
+    const int e = blockIdx.x / C::NU;
+    int rem = u, b = 0;
+#pragma unroll
+    for (int bb = 0; bb < C::NB - 1; ++bb)
+        if (b == bb && rem >= C::n(bb, 1) * C::n(bb, 2)) { rem -= C::n(bb, 1) * C::n(bb, 2); b = bb + 1; }
+    int n2b = C::n(0, 1);
+#pragma unroll
+    for (int bb = 1; bb < C::NB; ++bb)
+        if (b == bb) n2b = C::n(bb, 1);
+    const int j2 = rem % n2b, j3 = rem / n2b;
+
+    double *sF = smem + C::OFF_F;
+    for (int idx = tid; idx < 4 * KF * KF; idx += AFF2_THREADS) {
+        const int rs = idx / (KF * KF), q = idx - rs * KF * KF, i = q / KF, j = q - i * KF;
+        sF[idx] = args.tables[TAB_F + (rs * KT + i) * KT + j];
+    }
+    if (tid == 0) {
+        double J[3][3], D[6], Cm[6];
+        dev_jacobian(args.kind[e], args.params + 24LL * e, 0.5, 0.5, 0.5, J);
+        const double det = dev_metrics(J, D, Cm);
+        dev_fields(S, det, D, Cm, 1.0, args.coef ? args.coef[e] : 1.0, s_field);
+        if (u == 0) {
+            if (!(det > 0.0)) atomicOr(args.status + e, 1);
+            if (args.kind[e] > 2) atomicOr(args.status + e, 2);  // gram.py:170-174
+        }
+    }
+    __syncthreads();
+    // Bs_h[a][K = (i2, i3)] for every test block a >= b
+    if constexpr (C::NB == 1) {
+        aff_bsum<S, P, 0, 0>(smem, s_field, j2, j3);
+    } else {
+        if (b == 0) {
+            aff_bsum<S, P, 0, 0>(smem, s_field, j2, j3);
+            aff_bsum<S, P, 1, 0>(smem, s_field, j2, j3);
+            aff_bsum<S, P, 2, 0>(smem, s_field, j2, j3);
+        } else if (b == 1) {
+            aff_bsum<S, P, 1, 1>(smem, s_field, j2, j3);
+            aff_bsum<S, P, 2, 1>(smem, s_field, j2, j3);
+        } else {
+            aff_bsum<S, P, 2, 2>(smem, s_field, j2, j3);
+        }
+    }
+    __syncthreads();
+    double *__restrict__ outE = args.out + (long long)e * args.P;
+    const int epar = (int)((reinterpret_cast<size_t>(outE) >> 3) & 1);
+    int buf = 0;
+    if constexpr (C::NB == 1) {
+        aff_block<S, P, 0, 0>(smem, outE, epar, j2, j3, buf);
+    } else {
+        if (b == 0) {
+            aff_block<S, P, 0, 0>(smem, outE, epar, j2, j3, buf);
+            aff_block<S, P, 1, 0>(smem, outE, epar, j2, j3, buf);
+            aff_block<S, P, 2, 0>(smem, outE, epar, j2, j3, buf);
+        } else if (b == 1) {
+            aff_block<S, P, 1, 1>(smem, outE, epar, j2, j3, buf);
+            aff_block<S, P, 2, 1>(smem, outE, epar, j2, j3, buf);
+        } else {
+            aff_block<S, P, 2, 2>(smem, outE, epar, j2, j3, buf);
+        }
+    }
+    bulk_wait_all();
+}
+
+}  // namespace hxg

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/hexgram_b200.h"
+#include "hxg_affine_v2.cuh"
 #include "hxg_general_v2.cuh"
 #include "hxg_kernels.cuh"
 #include "hxg_v2_launch.h"
@@ -359,6 +360,33 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
     if (cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
 
     if (path == AFFINE) {
+        const char *force = getenv("HXG_FORCE_GENERIC");
+        if (p1 == p2 && p2 == p3 && !(force && force[0] == '1')) {
+            // compile-time specialized kernel (isotropic p <= 10), chunked below 2^31 blocks
+            const long long units = P.nb == 1 ? (long long)P.n[0][1] * P.n[0][2]
+                                              : (long long)P.n[0][1] * P.n[0][2] + P.n[1][1] * P.n[1][2] +
+                                                    P.n[2][1] * P.n[2][2];
+            const long long maxE = std::max<long long>(1, ((1ll << 31) - 1) / units);
+            int r = 0;
+            for (long long e0 = 0; e0 < E && r == 0; e0 += maxE) {
+                AffV2Args a2;
+                a2.kind = kind + e0;
+                a2.params = params + 24 * e0;
+                a2.coef = coef ? coef + e0 : nullptr;
+                a2.tables = tables;
+                a2.out = out + e0 * Pk;
+                a2.status = status + e0;
+                a2.P = Pk;
+                a2.E = (int)std::min<long long>(maxE, E - e0);
+                switch (space) {
+                case H1: r = launch_aff_H1(p1, a2, st); break;
+                case HCURL: r = launch_aff_hcurl(p1, a2, st); break;
+                case HDIV: r = launch_aff_hdiv(p1, a2, st); break;
+                default: r = launch_aff_l2(p1, a2, st); break;
+                }
+            }
+            if (r <= 0) return r == 0 ? HXG_OK : HXG_ERR_CUDA;
+        }
         AffArgs a;
         memset(&a, 0, sizeof(a));
         a.plan = P;

@@ -2,6 +2,7 @@
 // Specialized general-map kernels for space HDIV, isotropic orders p = 1..10, L = p + 1.
 #include "hxg_general_v2.cuh"
 #include "hxg_general_v3.cuh"
+#include "hxg_affine_v2.cuh"
 #include "hxg_v2_launch.h"
 
 namespace hxg {
@@ -45,6 +46,34 @@ int launch_v2_hdiv(int p, const V2Args &a, cudaStream_t st)
 {
     switch (p) {
 #define HXG_CASE(PP) case PP: return launch_one<PP>(a, a.E * units_one<PP>(), st);
+        HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
+        HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#undef HXG_CASE
+    }
+    return 1;
+}
+
+template <int P>
+static int launch_aff_one(const AffV2Args &a, cudaStream_t st)
+{
+    using C = AffCfg<HDIV, P>;
+    if constexpr (C::SMEM_BYTES > 200 * 1024) {
+        return 1;  // row images do not fit: runtime-generic affine kernel
+    }
+    auto k = affine_v2_kernel<HDIV, P>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
+        return -5;
+    const long long grid = (long long)a.E * C::NU;
+    if (grid >= (1ll << 31)) return -6;
+    k<<<(int)grid, AFF2_THREADS, C::SMEM_BYTES, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// specialized constant-Jacobian kernel; returns 1 if none exists for p
+int launch_aff_hdiv(int p, const AffV2Args &a, cudaStream_t st)
+{
+    switch (p) {
+#define HXG_CASE(PP) case PP: return launch_aff_one<PP>(a, st);
         HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
         HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
 #undef HXG_CASE

@@ -5,8 +5,13 @@
 
 namespace hxg {
 struct V2Args;
+struct AffV2Args;
 int launch_v2_H1(int p, const V2Args &a, cudaStream_t st);
 int launch_v2_hcurl(int p, const V2Args &a, cudaStream_t st);
 int launch_v2_hdiv(int p, const V2Args &a, cudaStream_t st);
 int launch_v2_l2(int p, const V2Args &a, cudaStream_t st);
+int launch_aff_H1(int p, const AffV2Args &a, cudaStream_t st);
+int launch_aff_hcurl(int p, const AffV2Args &a, cudaStream_t st);
+int launch_aff_hdiv(int p, const AffV2Args &a, cudaStream_t st);
+int launch_aff_l2(int p, const AffV2Args &a, cudaStream_t st);
 }  // namespace hxg
