@@ -89,6 +89,22 @@ struct V3Args {
     int split;  // CTAs per element
 };
 
+// stage-B groups listed per h: gl[h][q] = q-th g with g_h[g] == h, or -1
+struct GList {
+    int g[MAXH][MAXG];
+};
+__host__ __device__ constexpr GList make_glist(const CPair &pp)
+{
+    GList L{};
+    for (int h = 0; h < MAXH; ++h) {
+        int q = 0;
+        for (int k = 0; k < MAXG; ++k) L.g[h][k] = -1;
+        for (int g = 0; g < pp.ng; ++g)
+            if (pp.g_h[g] == h) L.g[h][q++] = g;
+    }
+    return L;
+}
+
 // explicit shared-memory load (ordered after the warp barrier that publishes B_h)
 __device__ __forceinline__ double lds_f64(const double *p)
 {
@@ -104,6 +120,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
 {
     using C = V3Cfg<S, P, L>;
     constexpr CPair pp = make_pair_plan(S, A, B);
+    constexpr GList GL = make_glist(pp);
     constexpr int LP = C::LP, L3 = C::L3, N = C::N, SW = C::SW;
     constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1);
     constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1);
@@ -126,25 +143,41 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
         sP[o] = n < L ? sT[(fr * KT + i3 + sha2) * LP + n] * sT[(fs * KT + j3 + shb2) * LP + n] : 0.0;
     }
     __syncwarp();
+    constexpr int NPASS = (L * L + 31) / 32;  // metric points per lane
 #pragma unroll
     for (int g = 0; g < pp.ng; ++g) {
+        double acc[NPASS];
 #pragma unroll
-        for (int lm0 = 0; lm0 < L * L; lm0 += 32) {
-            const int lm = lm0 + lane;
-            if (lm < L * L) {
-                double acc = 0.0;
+        for (int q = 0; q < NPASS; ++q) acc[q] = 0.0;
 #pragma unroll
-                for (int t = 0; t < pp.nt; ++t) {
-                    if (pp.t_g[t] != g) continue;
-                    const double *Mf = M + pp.t_field[t] * L3 + lm;
-                    const double *pt = sP + t * 8;
-                    double s = 0.0;
+        for (int t = 0; t < pp.nt; ++t) {
+            if (pp.t_g[t] != g) continue;
+            const double *Mf = M + pp.t_field[t] * L3;
+            const double *pt = sP + t * 8;
+            double v[NPASS][L];
 #pragma unroll
-                    for (int n = 0; n < L; ++n) s = fma(__ldg(Mf + n * L * L), pt[n], s);
-                    acc += pp.t_sign[t] > 0 ? s : -s;
+            for (int q = 0; q < NPASS; ++q) {
+                const int lm = cmin(lane + 32 * q, L * L - 1);
+#pragma unroll
+                for (int n = 0; n < L; ++n) v[q][n] = __ldg(Mf + n * L * L + lm);
+            }
+#pragma unroll
+            for (int q = 0; q < NPASS; ++q) {
+                double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                for (int n = 0; n < L; n += 2) {
+                    s0 = fma(v[q][n], pt[n], s0);
+                    if (n + 1 < L) s1 = fma(v[q][n + 1], pt[n + 1], s1);
                 }
+                acc[q] += pp.t_sign[t] > 0 ? (s0 + s1) : -(s0 + s1);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NPASS; ++q) {
+            const int lm = lane + 32 * q;
+            if (lm < L * L) {
                 const int l = lm / L, m = lm - l * L;
-                sA[(g * 8 + m) * 8 + l] = acc;
+                sA[(g * 8 + m) * 8 + l] = acc[q];
             }
         }
     }
@@ -227,21 +260,28 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
                 const int m = ks * 4 + t4;
                 Tb[fs][ks] = m < L ? sT[(fs * KT + j2 + shb1) * LP + m] : 0.0;
             }
+        // two h chains at a time: independent DMMA accumulators hide the DMMA latency
 #pragma unroll
-        for (int h = 0; h < pp.nh; ++h) {
-            double d0 = 0.0, d1 = 0.0;
+        for (int h0 = 0; h0 < pp.nh; h0 += 2) {
+            double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-            for (int g = 0; g < pp.ng; ++g) {
-                if (pp.g_h[g] != h) continue;
+            for (int q = 0; q < MAXG * LQ; ++q) {
 #pragma unroll
-                for (int ks = 0; ks < LQ; ++ks) {
-                    const double av = Ta[pp.g_fr[g]][ks] * Tb[pp.g_fs[g]][ks];
-                    const double bv = sA[(g * 8 + ks * 4 + t4) * 8 + g8];
-                    dmma_8x8x4_keep(d0, d1, av, bv, keep);
+                for (int c = 0; c < 2; ++c) {
+                    const int g = (h0 + c < MAXH) ? GL.g[h0 + c][q / LQ] : -1, ks = q % LQ;
+                    if (h0 + c < pp.nh && g >= 0) {
+                        const double av = Ta[pp.g_fr[g]][ks] * Tb[pp.g_fs[g]][ks];
+                        const double bv = sA[(g * 8 + ks * 4 + t4) * 8 + g8];
+                        dmma_8x8x4_keep(d[c][0], d[c][1], av, bv, keep);
+                    }
                 }
             }
-            sBw[(h * 8 + g8) * 8 + 2 * t4] = d0;
-            sBw[(h * 8 + g8) * 8 + 2 * t4 + 1] = d1;
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                if (h0 + c < pp.nh) {
+                    sBw[((h0 + c) * 8 + g8) * 8 + 2 * t4] = d[c][0];
+                    sBw[((h0 + c) * 8 + g8) * 8 + 2 * t4 + 1] = d[c][1];
+                }
         }
         __syncwarp();
         // staging buffer `buf` was last read by the bulk copies issued two rows-groups ago
@@ -255,35 +295,47 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
         double *srow = sS + g8 * SW + pad;
         // ---------------- stage C: contract xi1 on DMMA ----------------
         if constexpr (YF) {
-#pragma unroll kI2Unroll
-            for (int i2 = 0; i2 < n2a; ++i2) {
-                const double *base = sBw + i2 * 8;
-                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int i2 = 0; i2 < n2a; i2 += 2) {  // two tiles (i2, i2 + 1) in flight
+                double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
                 for (int ks = 0; ks < KSY; ++ks) {
-                    double y = Yc[ks][0] * base[Ro[ks][0]];
 #pragma unroll
-                    for (int q = 1; q < YQ; ++q) y = fma(Yc[ks][q], base[Ro[ks][q]], y);
-                    dmma_8x8x4_keep(d0, d1, y, R0[ks], keep);
+                    for (int c = 0; c < 2; ++c) {
+                        if (i2 + c < n2a) {
+                            const double *base = sBw + (i2 + c) * 8;
+                            double y = Yc[ks][0] * base[Ro[ks][0]];
+#pragma unroll
+                            for (int q = 1; q < YQ; ++q) y = fma(Yc[ks][q], base[Ro[ks][q]], y);
+                            dmma_8x8x4_keep(d[c][0], d[c][1], y, R0[ks], keep);
+                        }
+                    }
                 }
-                if (g8 < n1b) {
-                    if (2 * t4 < n1a) srow[i2 * n1a + 2 * t4] = d0;
-                    if (2 * t4 + 1 < n1a) srow[i2 * n1a + 2 * t4 + 1] = d1;
-                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    if (i2 + c < n2a && g8 < n1b) {
+                        if (2 * t4 < n1a) srow[(i2 + c) * n1a + 2 * t4] = d[c][0];
+                        if (2 * t4 + 1 < n1a) srow[(i2 + c) * n1a + 2 * t4 + 1] = d[c][1];
+                    }
             }
         } else {
 #pragma unroll
-            for (int i1 = 0; i1 < n1a; ++i1) {
-                double d0 = 0.0, d1 = 0.0;
+            for (int i1 = 0; i1 < n1a; i1 += 2) {  // two tiles (i1, i1 + 1) in flight
+                double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
                 for (int ks = 0; ks < NKS; ++ks) {
-                    const double bv = sT[Xo[ks] + i1 * LP] * sBw[Ro[ks][0]];
-                    dmma_8x8x4_keep(d0, d1, R0[ks], bv, keep);
+                    const double bb = sBw[Ro[ks][0]];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+                        if (i1 + c < n1a)
+                            dmma_8x8x4_keep(d[c][0], d[c][1], R0[ks], sT[Xo[ks] + (i1 + c) * LP] * bb, keep);
                 }
-                if (g8 < n1b) {  // columns i2 = 2 t4, 2 t4 + 1
-                    if (2 * t4 < n2a) srow[(2 * t4) * n1a + i1] = d0;
-                    if (2 * t4 + 1 < n2a) srow[(2 * t4 + 1) * n1a + i1] = d1;
-                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    if (i1 + c < n1a && g8 < n1b) {  // columns i2 = 2 t4, 2 t4 + 1
+                        if (2 * t4 < n2a) srow[(2 * t4) * n1a + i1 + c] = d[c][0];
+                        if (2 * t4 + 1 < n2a) srow[(2 * t4 + 1) * n1a + i1 + c] = d[c][1];
+                    }
             }
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
