@@ -57,7 +57,7 @@ struct V3Cfg {
     static constexpr int W_A = W_P + NT * 8;            // [NG][8][8] Abar (rows m, cols l; zero padded)
     static constexpr int W_B = W_A + NG * 64;           // [NH][8][8] B_h (rows i2, cols l)
     static constexpr int W_S = W_B + NH * 64;           // [2][8][SW] staging
-    static constexpr int W_TOT = W_S + 2 * 8 * SW;
+    static constexpr int W_TOT = W_S + 2 * C2::N1 * SW;  // [2][N1][SW] staging
     static constexpr int OFF_T = 0;                     // CTA-shared [2][KT][LP]
     static constexpr int OFF_W = 2 * KT * LP;
     static constexpr int SMEM_BYTES = (OFF_W + V3_WARPS * W_TOT) * 8 + 16;
@@ -76,7 +76,8 @@ struct V3Cfg {
 #ifdef HXG_V3_MINB
     static constexpr int MINB = HXG_V3_MINB;
 #else
-    static constexpr int MINB = cmin(8, (228 * 1024) / (SMEM_BYTES + 1024));
+    // CTAs per SM: 5 (<= 102 registers) measured best for H1/H(curl)/H(div), 4 for L2
+    static constexpr int MINB = cmin(S == L2 ? 4 : 5, (228 * 1024) / (SMEM_BYTES + 1024));
 #endif
 };
 
@@ -288,7 +289,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
         asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
         __syncwarp();
 
-        double *sS = W + C::W_S + buf * 8 * SW;
+        double *sS = W + C::W_S + buf * C::C2::N1 * SW;
         const int J = offB + g8 + n1b * (j2 + n2b * j3);  // row of this lane's j1 = g8
         const int goff = J * N - J * (J - 1) / 2 - J + I0;
         const int pad = (epar + goff) & 1;
@@ -395,8 +396,8 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
         }
 #endif
 #if HXG_V3_DEBUG2 & 4
-        const double *sSl = W + C::W_S + (buf ^ 1) * 8 * SW;
-        for (int q = lane; q < 8 * SW; q += 32) hxg_dbg[3328 + q] = sSl[q];
+        const double *sSl = W + C::W_S + (buf ^ 1) * C::C2::N1 * SW;
+        for (int q = lane; q < C::C2::N1 * SW; q += 32) hxg_dbg[3328 + q] = sSl[q];
 #endif
     }
 #endif
