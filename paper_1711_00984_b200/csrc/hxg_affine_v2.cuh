@@ -5,9 +5,8 @@
 //   G[J, I] = sum_h F_h[i1 + sa][j1 + sb] * Bs_h[a, i2, i3]     (<= 4 FMAs per entry)
 //   Bs_h    = sum_{g in h} F_g[i2][j2] * sum_{t in g} sign * field_t * F_t[i3][j3]
 // and the kernel is bound by the packed-output write.  One CTA owns the n1b
-// packed rows J = (j1, j2, j3, b); threads (j1, i1, K-slot) evaluate one entry
-// per column group K = (i2, i3) into a shared-memory row image, which is sent
-// to HBM with one bulk copy (cp.async.bulk) per row and test block.
+// packed rows J = (j1, j2, j3, b): the Bs sums go to shared memory, then each
+// warp streams whole packed rows to HBM with coalesced stores (aff_rows).
 #pragma once
 #include "hxg_common.cuh"
 #include "hxg_general_v2.cuh"
@@ -45,11 +44,9 @@ struct AffCfg {
     static constexpr int NK = cmax(n(0, 1) * n(0, 2), NB > 1 ? cmax(n(1, 1) * n(1, 2), n(2, 1) * n(2, 2)) : 0);
     static constexpr int BMAX = cmax(blk(0), NB > 1 ? cmax(blk(1), blk(2)) : 0);
     static constexpr int KF = P + 2;                 // F-table index range needed
-    static constexpr int SWA = ((BMAX + 2) / 2) * 2;  // staging row stride (>= BMAX + 1, even)
     static constexpr int OFF_F = 0;                  // [4][KF][KF]
     static constexpr int OFF_B = OFF_F + 4 * KF * KF;  // [NB][NK][4]
-    static constexpr int OFF_S = ((OFF_B + NB * NK * 4 + 1) / 2) * 2;  // [2][N1][SWA]
-    static constexpr int SMEM_BYTES = (OFF_S + 2 * N1 * SWA) * 8;
+    static constexpr int SMEM_BYTES = (OFF_B + NB * NK * 4) * 8;
     __host__ __device__ static constexpr int units()
     {
         int u = 0;
@@ -59,82 +56,50 @@ struct AffCfg {
     static constexpr int NU = units();
 };
 
+// Direct variant: warp w writes packed rows j1 = w, w + 4, ...; lane (kq, i1) keeps its
+// test digit i1 (and hence its F factors) fixed and walks column groups K with stride
+// KW = 32 / n1a, so each warp store covers KW * n1a consecutive doubles of the row.
 template <int S, int P, int A, int B>
-__device__ __forceinline__ void aff_block(double *smem, double *__restrict__ outE, int epar, int j2,
-                                          int j3, int &buf)
+__device__ __forceinline__ void aff_rows(const double *smem, double *__restrict__ outE, int j2, int j3)
 {
     using C = AffCfg<S, P>;
     constexpr CPair pp = make_pair_plan(S, A, B);
-    constexpr int KF = C::KF, SWA = C::SWA, N = C::N;
+    constexpr int KF = C::KF, N = C::N;
     constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1), n3a = C::n(A, 2);
     constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1);
     constexpr int sha0 = sh_of(S, A, 0), shb0 = sh_of(S, B, 0);
     constexpr int offA = C::off(A), offB = C::off(B);
-    constexpr int TPK = n1a * n1b;                       // threads per column group
-    constexpr int KS = AFF2_THREADS / TPK;               // column groups in flight
+    constexpr int KW = n1a <= 32 ? 32 / n1a : 1;
     const double *sF = smem + C::OFF_F;
     const double *sBs = smem + C::OFF_B + A * C::NK * 4;
-    double *sS = smem + C::OFF_S + buf * C::N1 * SWA;
-    const int tid = threadIdx.x;
-
-    const int Kp = j2 + n2b * j3;                        // trial column group
-    const int K0 = (A == B) ? Kp : 0;                    // first needed test group
-    const int nK = n2a * n3a - K0;
-    const int I0 = offA + K0 * n1a;                      // first column of the image
-
-    // this thread's (j1, i1) and its F factors
-    const int slot = tid / TPK, r = tid - slot * TPK;
-    const int j1 = r / n1a, i1 = r - j1 * n1a;
-    double Fr[MAXH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane / n1a, i1 = lane - kq * n1a;
+    const bool act = kq < KW;
+    const int Kp = j2 + n2b * j3;
+    const int K0 = (A == B) ? Kp : 0;
+    for (int j1 = warp; j1 < n1b; j1 += AFF2_THREADS / 32) {
+        double Fr[MAXH];
 #pragma unroll
-    for (int h = 0; h < MAXH; ++h)
-        Fr[h] = (h < pp.nh && slot < KS)
-                    ? sF[((2 * pp.h_fr[h] + pp.h_fs[h]) * KF + i1 + sha0) * KF + j1 + shb0]
-                    : 0.0;
-    if (slot < KS) {
+        for (int h = 0; h < MAXH; ++h)
+            Fr[h] = h < pp.nh ? sF[((2 * pp.h_fr[h] + pp.h_fs[h]) * KF + i1 + sha0) * KF + j1 + shb0] : 0.0;
         const int J = offB + j1 + n1b * Kp;
-        const int goff = J * N - J * (J - 1) / 2 - J + I0;
-        const int pad = (epar + goff) & 1;
-        double *srow = sS + j1 * SWA + pad + i1;
-        for (int k = slot; k < nK; k += KS) {
-            const double2 b01 = *reinterpret_cast<const double2 *>(sBs + (K0 + k) * 4);
-            double v = Fr[0] * b01.x;
-            if (pp.nh > 1) v = fma(Fr[1], b01.y, v);
-            if (pp.nh > 2) {
-                const double2 b23 = *reinterpret_cast<const double2 *>(sBs + (K0 + k) * 4 + 2);
-                v = fma(Fr[2], b23.x, v);
-                if (pp.nh > 3) v = fma(Fr[3], b23.y, v);
+        double *rowp = outE + (J * N - J * (J - 1) / 2 - J);  // &G(J, 0)
+        if (act) {
+#pragma unroll 4
+            for (int K = K0 + kq; K < n2a * n3a; K += KW) {
+                const int I = offA + K * n1a + i1;
+                const double2 b01 = *reinterpret_cast<const double2 *>(sBs + K * 4);
+                double v = Fr[0] * b01.x;
+                if (pp.nh > 1) v = fma(Fr[1], b01.y, v);
+                if (pp.nh > 2) {
+                    const double2 b23 = *reinterpret_cast<const double2 *>(sBs + K * 4 + 2);
+                    v = fma(Fr[2], b23.x, v);
+                    if (pp.nh > 3) v = fma(Fr[3], b23.y, v);
+                }
+                if (I >= J) __stcs(rowp + I, v);
             }
-            srow[k * n1a] = v;
         }
     }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid < n1b) {
-        const int J = offB + tid + n1b * Kp;
-        const int goff = J * N - J * (J - 1) / 2 - J + I0;
-        const int pad = (epar + goff) & 1;
-        const int ncols = nK * n1a;
-        const int cs = J > I0 ? J - I0 : 0;
-        if (cs < ncols) {
-            const double *src = sS + tid * SWA + pad + cs;
-            double *dst = outE + goff + cs;
-            int len = ncols - cs;
-            if (reinterpret_cast<size_t>(dst) & 8) {
-                __stcs(dst, *src);
-                ++dst;
-                ++src;
-                --len;
-            }
-            if (len & 1) __stcs(dst + len - 1, src[len - 1]);
-            if (len >= 2) bulk_s2g(dst, src, (len & ~1) * 8);
-        }
-        bulk_commit();
-        // the other staging buffer is rewritten by the next block: its copies must have read it
-        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-    }
-    __syncthreads();
-    buf ^= 1;
 }
 
 // Bs_h[A][K] for one (test block A, trial block B) pair
@@ -221,23 +186,20 @@ __global__ void __launch_bounds__(AFF2_THREADS) affine_v2_kernel(const __grid_co
     }
     __syncthreads();
     double *__restrict__ outE = args.out + (long long)e * args.P;
-    const int epar = (int)((reinterpret_cast<size_t>(outE) >> 3) & 1);
-    int buf = 0;
     if constexpr (C::NB == 1) {
-        aff_block<S, P, 0, 0>(smem, outE, epar, j2, j3, buf);
+        aff_rows<S, P, 0, 0>(smem, outE, j2, j3);
     } else {
         if (b == 0) {
-            aff_block<S, P, 0, 0>(smem, outE, epar, j2, j3, buf);
-            aff_block<S, P, 1, 0>(smem, outE, epar, j2, j3, buf);
-            aff_block<S, P, 2, 0>(smem, outE, epar, j2, j3, buf);
+            aff_rows<S, P, 0, 0>(smem, outE, j2, j3);
+            aff_rows<S, P, 1, 0>(smem, outE, j2, j3);
+            aff_rows<S, P, 2, 0>(smem, outE, j2, j3);
         } else if (b == 1) {
-            aff_block<S, P, 1, 1>(smem, outE, epar, j2, j3, buf);
-            aff_block<S, P, 2, 1>(smem, outE, epar, j2, j3, buf);
+            aff_rows<S, P, 1, 1>(smem, outE, j2, j3);
+            aff_rows<S, P, 2, 1>(smem, outE, j2, j3);
         } else {
-            aff_block<S, P, 2, 2>(smem, outE, epar, j2, j3, buf);
+            aff_rows<S, P, 2, 2>(smem, outE, j2, j3);
         }
     }
-    bulk_wait_all();
 }
 
 }  // namespace hxg
