@@ -544,8 +544,34 @@ int hxg_expand_full(int N, int E, const double *packed, double *full, void *stre
 }
 
 // Host-buffer entry: the reference's calling convention (numpy in, numpy out).
-// Inputs are copied once; the batch is integrated in chunks on two streams so
-// that the device->host copy of chunk i overlaps the integration of chunk i+1.
+// Inputs are copied once; the batch is integrated in ~256 MB output chunks on two
+// streams so that the device->host copy of chunk i overlaps the integration of
+// chunk i+1.  Device buffers and streams live in a per-device context that grows
+// on demand and is reused by later calls (no cudaMalloc/cudaFree per call).
+namespace {
+struct HostCtx {
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t inputs_ready = nullptr;
+    void *buf[9] = {nullptr};
+    size_t cap[9] = {0};
+    void *get(int k, size_t bytes, bool &ok)
+    {
+        if (bytes == 0) return nullptr;
+        if (cap[k] < bytes) {
+            if (buf[k]) cudaFree(buf[k]);
+            buf[k] = nullptr;
+            cap[k] = 0;
+            if (cudaMalloc(&buf[k], bytes) != cudaSuccess) { ok = false; return nullptr; }
+            cap[k] = bytes;
+        }
+        return buf[k];
+    }
+};
+HostCtx g_host_ctx[64];
+}  // namespace
+
 int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, int E,
                           const int *kind, const double *params, const double *coef, double *out,
                           int *status)
@@ -557,67 +583,55 @@ int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, in
     SpacePlan P;
     rc = build_plan(space, p1, p2, p3, P);
     if (rc != HXG_OK) return rc;
-    const long long Pk = (long long)P.N * (P.N + 1) / 2;
-    const size_t out_bytes_el = (size_t)Pk * sizeof(double);
-    // chunk so that one output buffer is ~256 MB
-    long long ch = std::max<long long>(1, (256ll << 20) / (long long)out_bytes_el);
-    ch = std::min<long long>(ch, E);
-    cudaStream_t s[2];
-    cudaEvent_t inputs_ready;
-    int *d_kind = nullptr, *d_status = nullptr;
-    double *d_params = nullptr, *d_coef = nullptr, *d_tab = nullptr, *d_out[2] = {nullptr, nullptr};
-    void *d_ws[2] = {nullptr, nullptr};
-    size_t ws = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return HXG_ERR_CUDA;
+    HostCtx &cx = g_host_ctx[dev];
+    std::lock_guard<std::mutex> lock(cx.mu);
     bool ok = true;
     auto chk = [&](cudaError_t e) { if (e != cudaSuccess) ok = false; };
-    chk(cudaStreamCreateWithFlags(&s[0], cudaStreamNonBlocking));
-    chk(cudaStreamCreateWithFlags(&s[1], cudaStreamNonBlocking));
-    chk(cudaEventCreateWithFlags(&inputs_ready, cudaEventDisableTiming));
-    chk(cudaMalloc(&d_kind, sizeof(int) * (size_t)E));
-    chk(cudaMalloc(&d_status, sizeof(int) * (size_t)E));
-    chk(cudaMalloc(&d_params, sizeof(double) * 24 * (size_t)E));
-    if (coef) chk(cudaMalloc(&d_coef, sizeof(double) * (size_t)E));
-    chk(cudaMalloc(&d_tab, sizeof(double) * TAB_TOTAL));
-    for (int i = 0; i < 2; ++i) chk(cudaMalloc(&d_out[i], out_bytes_el * (size_t)ch));
-    if (path == GENERAL) {
-        ws = hxg_workspace_size(space, path, p1, p2, p3, L, (int)ch);
-        for (int i = 0; i < 2; ++i) chk(cudaMalloc(&d_ws[i], ws));
+    if (!cx.init) {
+        chk(cudaStreamCreateWithFlags(&cx.s[0], cudaStreamNonBlocking));
+        chk(cudaStreamCreateWithFlags(&cx.s[1], cudaStreamNonBlocking));
+        chk(cudaEventCreateWithFlags(&cx.inputs_ready, cudaEventDisableTiming));
+        if (!ok) return HXG_ERR_CUDA;
+        cx.init = true;
     }
-    if (ok) {
-        chk(cudaMemcpyAsync(d_kind, kind, sizeof(int) * (size_t)E, cudaMemcpyHostToDevice, s[0]));
-        chk(cudaMemcpyAsync(d_params, params, sizeof(double) * 24 * (size_t)E, cudaMemcpyHostToDevice, s[0]));
-        if (coef) chk(cudaMemcpyAsync(d_coef, coef, sizeof(double) * (size_t)E, cudaMemcpyHostToDevice, s[0]));
-        const int trc = hxg_make_tables(L <= LT ? std::max(L, 1) : 1, nullptr, nullptr, d_tab, s[0]);
-        if (trc != HXG_OK) rc = trc;
-        chk(cudaEventRecord(inputs_ready, s[0]));
-        chk(cudaStreamWaitEvent(s[1], inputs_ready, 0));
-        int i = 0;
-        for (long long e0 = 0; e0 < E && ok && rc == HXG_OK; e0 += ch, ++i) {
-            const int ne = (int)std::min<long long>(ch, E - e0);
-            cudaStream_t st = s[i & 1];
-            rc = hxg_gram_batched(space, path, p1, p2, p3, L, ne, d_kind + e0, d_params + 24 * e0,
-                                  d_coef ? d_coef + e0 : nullptr, nullptr, d_tab, d_out[i & 1],
-                                  d_status + e0, d_ws[i & 1], ws, st);
-            if (rc != HXG_OK) break;
-            chk(cudaMemcpyAsync(out + e0 * Pk, d_out[i & 1], out_bytes_el * (size_t)ne,
-                                cudaMemcpyDeviceToHost, st));
-        }
-        chk(cudaStreamSynchronize(s[0]));
-        chk(cudaStreamSynchronize(s[1]));
-        if (status && ok) chk(cudaMemcpy(status, d_status, sizeof(int) * (size_t)E, cudaMemcpyDeviceToHost));
+    const long long Pk = (long long)P.N * (P.N + 1) / 2;
+    const size_t out_bytes_el = (size_t)Pk * sizeof(double);
+    long long ch = std::max<long long>(1, (256ll << 20) / (long long)out_bytes_el);
+    ch = std::min<long long>(ch, E);
+    size_t ws = path == GENERAL ? hxg_workspace_size(space, path, p1, p2, p3, L, (int)ch) : 0;
+    int *d_kind = (int *)cx.get(0, sizeof(int) * (size_t)E, ok);
+    int *d_status = (int *)cx.get(1, sizeof(int) * (size_t)E, ok);
+    double *d_params = (double *)cx.get(2, sizeof(double) * 24 * (size_t)E, ok);
+    double *d_coef = coef ? (double *)cx.get(3, sizeof(double) * (size_t)E, ok) : nullptr;
+    double *d_tab = (double *)cx.get(4, sizeof(double) * TAB_TOTAL, ok);
+    double *d_out[2] = {(double *)cx.get(5, out_bytes_el * (size_t)ch, ok),
+                        (double *)cx.get(6, out_bytes_el * (size_t)ch, ok)};
+    void *d_ws[2] = {cx.get(7, ws, ok), cx.get(8, ws, ok)};
+    if (!ok) return HXG_ERR_CUDA;
+    cudaStream_t *s = cx.s;
+    chk(cudaMemcpyAsync(d_kind, kind, sizeof(int) * (size_t)E, cudaMemcpyHostToDevice, s[0]));
+    chk(cudaMemcpyAsync(d_params, params, sizeof(double) * 24 * (size_t)E, cudaMemcpyHostToDevice, s[0]));
+    if (coef) chk(cudaMemcpyAsync(d_coef, coef, sizeof(double) * (size_t)E, cudaMemcpyHostToDevice, s[0]));
+    rc = hxg_make_tables(path == GENERAL ? L : 1, nullptr, nullptr, d_tab, s[0]);
+    chk(cudaEventRecord(cx.inputs_ready, s[0]));
+    chk(cudaStreamWaitEvent(s[1], cx.inputs_ready, 0));
+    int i = 0;
+    for (long long e0 = 0; e0 < E && ok && rc == HXG_OK; e0 += ch, ++i) {
+        const int ne = (int)std::min<long long>(ch, E - e0);
+        cudaStream_t st = s[i & 1];
+        rc = hxg_gram_batched(space, path, p1, p2, p3, L, ne, d_kind + e0, d_params + 24 * e0,
+                              d_coef ? d_coef + e0 : nullptr, nullptr, d_tab, d_out[i & 1],
+                              d_status + e0, d_ws[i & 1], ws, st);
+        if (rc != HXG_OK) break;
+        chk(cudaMemcpyAsync(out + e0 * Pk, d_out[i & 1], out_bytes_el * (size_t)ne,
+                            cudaMemcpyDeviceToHost, st));
     }
-    cudaFree(d_kind);
-    cudaFree(d_status);
-    cudaFree(d_params);
-    cudaFree(d_coef);
-    cudaFree(d_tab);
-    cudaFree(d_out[0]);
-    cudaFree(d_out[1]);
-    cudaFree(d_ws[0]);
-    cudaFree(d_ws[1]);
-    cudaEventDestroy(inputs_ready);
-    cudaStreamDestroy(s[0]);
-    cudaStreamDestroy(s[1]);
+    chk(cudaStreamSynchronize(s[0]));
+    chk(cudaStreamSynchronize(s[1]));
+    if (status && ok && rc == HXG_OK)
+        chk(cudaMemcpy(status, d_status, sizeof(int) * (size_t)E, cudaMemcpyDeviceToHost));
     if (rc != HXG_OK) return rc;
     return ok ? HXG_OK : HXG_ERR_CUDA;
 }
