@@ -447,6 +447,95 @@ def run_ours(args, wl, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_sweep(args, world, rank, local):
+    """BASELINE config 5: H1/H(curl)/H(div), p_test = 2..10 (L = p + 1), affine and
+    trilinear maps, E_p = floor(budget / B(p)) elements (<= 100 GB of packed fp64
+    output), strong scaling over ranks (each rank integrates E_p / N elements).
+    Reports elements/s, Gram-entries/s, roofline fraction per point and the
+    fitted exponent of time-per-element vs p (p^7 general, p^6 affine expected
+    for the FP64-bound points; HBM-bound points scale with the output, ~p^6)."""
+    import torch
+
+    from paper_1711_00984_b200 import _native
+    from paper_1711_00984_b200.engine import get_engine
+    from paper_1711_00984_b200.inputs import affine_batch, packed_size, trilinear_batch
+
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    eng = get_engine(device)
+    lib = _native.lib()
+    hbm, _, fp64, _ = peaks()
+    budget = args.sweep_gb * 1e9
+    pmax_out = max(packed_size(sp, (pp, pp, pp)) for sp in ("H1", "Hcurl", "Hdiv")
+                   for pp in range(2, args.sweep_pmax + 1))
+    out_all = torch.empty(int(budget // 8) + pmax_out, dtype=torch.float64, device=device)
+    base_n = 4096
+    results = []
+    stream = torch.cuda.current_stream(device)
+    for path, maps in (("general", "trilinear"), ("affine", "affine")):
+        gen = trilinear_batch if maps == "trilinear" else affine_batch
+        base = gen(base_n, 4)  # seed 4 (config 5)
+        for space in ("H1", "Hcurl", "Hdiv"):
+            for p in range(2, args.sweep_pmax + 1):
+                orders = (p, p, p)
+                L = p + 1 if path == "general" else 1
+                Pk = packed_size(space, orders)
+                Eg = int(budget // (8 * Pk))
+                lo, hi = shard(Eg, world, rank)
+                E = hi - lo
+                # the seeded base batch tiled on the device to E elements (timing only;
+                # parity of these orders is covered by tests/test_gpu_parity.py)
+                reps = (E + base_n - 1) // base_n
+                kind = torch.as_tensor(base.kind).to(device).repeat(reps)[:E].contiguous()
+                params = torch.as_tensor(base.params).to(device).repeat(reps, 1)[:E].contiguous()
+                coef = torch.as_tensor(base.coef).to(device).repeat(reps)[:E].contiguous()
+                status = torch.zeros(E, dtype=torch.int32, device=device)
+                tab = eng.tables(L)
+                sc, pc = _native.SPACE_CODES[space], _native.PATH_CODES[path]
+                ws_bytes = lib.hxg_workspace_size(sc, pc, *orders, L, E)
+                ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
+                out = out_all[: E * Pk]
+                ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+
+                def step():
+                    rc = lib.hxg_gram_batched(sc, pc, *orders, L, E, ptr(kind), ptr(params), ptr(coef),
+                                              None, ptr(tab), ptr(out), ptr(status), ptr(ws), ws_bytes,
+                                              ctypes.c_void_p(stream.cuda_stream))
+                    assert rc == 0, rc
+
+                step()
+                torch.cuda.synchronize(device)
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                if world > 1:
+                    import torch.distributed as dist
+
+                    dist.barrier()
+                ev0.record(stream)
+                for _ in range(args.sweep_reps):
+                    step()
+                ev1.record(stream)
+                torch.cuda.synchronize(device)
+                sec = max_over_ranks(ev0.elapsed_time(ev1) / 1e3 / args.sweep_reps, world, device)
+                F, B, _ = algorithmic(space, orders, path, L)
+                t_roof = Eg / world * max(F / (fp64 * 1e12), B / (hbm * 1e9))
+                results.append({"space": space, "path": path, "p_test": p, "L": L, "elements": Eg,
+                                "elements_per_s": Eg / sec, "gram_entries_per_s": Eg * Pk / sec,
+                                "ms": sec * 1e3, "roofline_frac": t_roof / sec,
+                                "bound": "fp64" if F / fp64 / 1e3 > B / hbm else "hbm"})
+                del kind, params, coef, status, ws
+    fits = {}
+    for path in ("general", "affine"):
+        for space in ("H1", "Hcurl", "Hdiv"):
+            pts = [r for r in results if r["path"] == path and r["space"] == space]
+            x = np.log([r["p_test"] for r in pts])
+            y = np.log([1.0 / r["elements_per_s"] for r in pts])
+            fits[f"{space}/{path}"] = float(np.polyfit(x, y, 1)[0]) if len(pts) > 1 else None
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "mode": "sweep (BASELINE config 5)", "n_gpus": world,
+                          "scaling": "strong", "budget_gb_per_job": args.sweep_gb,
+                          "fitted_time_exponent_vs_p": fits, "points": results}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -459,10 +548,16 @@ def main():
     ap.add_argument("--suite", action=argparse.BooleanOptionalAction, default=True)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--sweep", action="store_true", help="BASELINE config 5 order sweep")
+    ap.add_argument("--sweep-gb", type=float, default=100.0)
+    ap.add_argument("--sweep-pmax", type=int, default=10)
+    ap.add_argument("--sweep-reps", type=int, default=2)
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     wl = WORKLOADS[args.workload]
-    if args.impl == "reference":
+    if args.sweep:
+        run_sweep(args, world, rank, local)
+    elif args.impl == "reference":
         run_reference(args, wl, world, rank)
     else:
         run_ours(args, wl, world, rank, local)
