@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1711_00984_b200.inputs import WORKLOADS, dim  # noqa: E402
+from paper_1711_00984_b200.inputs import ALL_WORKLOADS, WORKLOADS, dim  # noqa: E402
 
 METRIC = "Gram elements/sec per space & test order; achieved % of FP64/HBM roofline"
 UNIT = "elements/s"
@@ -542,7 +542,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="c2_h1_p5_general", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c2_h1_p5_general", choices=sorted(ALL_WORKLOADS))
     ap.add_argument("--elements", type=int, default=0, help="elements per GPU (default: config)")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--suite", action=argparse.BooleanOptionalAction, default=True)
@@ -554,7 +554,7 @@ def main():
     ap.add_argument("--sweep-reps", type=int, default=2)
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
-    wl = WORKLOADS[args.workload]
+    wl = ALL_WORKLOADS[args.workload]
     if args.sweep:
         run_sweep(args, world, rank, local)
     elif args.impl == "reference":

@@ -2,6 +2,7 @@
 // Specialized general-map kernels for space HDIV, isotropic orders p = 1..10, L = p + 1.
 #include "hxg_general_v2.cuh"
 #include "hxg_general_v3.cuh"
+#include "hxg_general_v4.cuh"
 #include "hxg_affine_v2.cuh"
 #include "hxg_v2_launch.h"
 
@@ -10,6 +11,27 @@ namespace hxg {
 template <int P>
 static int launch_one(const V2Args &a, int grid, cudaStream_t st)
 {
+    using C4 = V4Cfg<HDIV, P, P + 1>;
+    if constexpr (C4::OK && P >= 5) {
+        const char *v4env = getenv("HXG_USE_V4");
+        const bool use_v4 = P >= 8 || (v4env && v4env[0] == '1');
+        if (use_v4 && !(getenv("HXG_FORCE_V2") && getenv("HXG_FORCE_V2")[0] == '1')) {
+            auto k4 = general_v4_kernel<HDIV, P, P + 1>;
+            if (cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, C4::SMEM_BYTES) != cudaSuccess)
+                return -5;
+            V3Args b;
+            b.tables = a.tables;
+            b.metric = a.metric;
+            b.out = a.out;
+            b.P = a.P;
+            b.E = a.E;
+            const int want = 148 * C4::MINB * 4;
+            b.split = a.E >= want ? 1 : (want + a.E - 1) / a.E;
+            if (b.split > 32) b.split = 32;
+            k4<<<a.E * b.split, C4::THREADS, C4::SMEM_BYTES, st>>>(b);
+            return cudaGetLastError() == cudaSuccess ? 0 : -5;
+        }
+    }
     using C3 = V3Cfg<HDIV, P, P + 1>;
     if constexpr (C3::OK) {
         if (!(getenv("HXG_FORCE_V2") && getenv("HXG_FORCE_V2")[0] == '1')) {

@@ -123,3 +123,13 @@ def packed_size(space: str, orders) -> int:
 def sweep_elements(space: str, p: int, budget_bytes: float = 100e9) -> int:
     """Config 5: E_p = floor(budget / B(p)), B = 8 N(N+1)/2."""
     return int(budget_bytes // (8 * packed_size(space, (p, p, p))))
+
+
+# order-sweep points (BASELINE config 5), addressable by name for profiling
+SWEEP_WORKLOADS = {
+    f"c5_{sp.lower()}_p{p}_{path}": Workload(f"c5_{sp.lower()}_p{p}_{path}", sp, p, p + 1, path,
+                                             sweep_elements(sp, p), 4, maps)
+    for sp in ("H1", "Hcurl", "Hdiv") for p in range(2, 11)
+    for path, maps in (("general", "trilinear"), ("affine", "affine"))
+}
+ALL_WORKLOADS = {**WORKLOADS, **SWEEP_WORKLOADS}

@@ -254,7 +254,7 @@ def test_host_entry_matches_device_entry():
 
 
 @pytest.mark.parametrize("space", SPACES)
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 9])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10])
 def test_specialized_equals_generic(space, p, monkeypatch):
     """The compile-time specialized kernel (isotropic p, L = p + 1) and the
     runtime-generic kernel agree to 1e-12 on the same batch."""
@@ -265,11 +265,14 @@ def test_specialized_equals_generic(space, p, monkeypatch):
 
     b = trilinear_batch(3, 800 + p, variable_coef=True)
     spec, _ = gram_batched(space, (p, p, p), b.kind, b.params, b.coef)
+    monkeypatch.setenv("HXG_USE_V4", "1")  # tiled warp-unit kernel at orders it does not own
+    spec4, _ = gram_batched(space, (p, p, p), b.kind, b.params, b.coef)
+    monkeypatch.delenv("HXG_USE_V4")
     monkeypatch.setenv("HXG_FORCE_V2", "1")  # CTA-chunked specialization instead of warp units
     spec2, _ = gram_batched(space, (p, p, p), b.kind, b.params, b.coef)
     monkeypatch.setenv("HXG_FORCE_GENERIC", "1")
     gen, _ = gram_batched(space, (p, p, p), b.kind, b.params, b.coef)
     torch.cuda.synchronize()
-    for got in (spec, spec2):
+    for got in (spec, spec4, spec2):
         rel = torch.linalg.norm(got - gen, dim=1) / torch.linalg.norm(gen, dim=1)
         assert float(rel.max()) <= TOL

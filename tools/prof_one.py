@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from bench import DeviceStep  # noqa: E402
-from paper_1711_00984_b200.inputs import WORKLOADS  # noqa: E402
+from paper_1711_00984_b200.inputs import ALL_WORKLOADS as WORKLOADS  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("workload")
