@@ -255,8 +255,12 @@ class DeviceStep:
                                          *wl.orders, self.L, E)
         self.ws_bytes = ws
         self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
-        self.full_metric = ws >= self.lib.hxg_workspace_size(self.sc, 0, *wl.orders, self.L, E) \
-            if wl.path == "general" else True
+        # p <= 3 runs one fused kernel (geometry in the contraction kernel): time the
+        # whole hxg_gram_batched call; otherwise time metric and contraction separately
+        self.fused = wl.path == "general" and wl.p <= 3
+        self.full_metric = (not self.fused) and (
+            ws >= self.lib.hxg_workspace_size(self.sc, 0, *wl.orders, self.L, E)
+            if wl.path == "general" else True)
         self.flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
         self.launches_per_step = 0
 
@@ -526,10 +530,12 @@ def run_sweep(args, world, rank, local):
     fits = {}
     for path in ("general", "affine"):
         for space in ("H1", "Hcurl", "Hdiv"):
-            pts = [r for r in results if r["path"] == path and r["space"] == space]
-            x = np.log([r["p_test"] for r in pts])
-            y = np.log([1.0 / r["elements_per_s"] for r in pts])
-            fits[f"{space}/{path}"] = float(np.polyfit(x, y, 1)[0]) if len(pts) > 1 else None
+            for pmin in (2, 5):
+                pts = [r for r in results if r["path"] == path and r["space"] == space
+                       and r["p_test"] >= pmin]
+                x = np.log([r["p_test"] for r in pts])
+                y = np.log([1.0 / r["elements_per_s"] for r in pts])
+                fits[f"{space}/{path}/p>={pmin}"] = float(np.polyfit(x, y, 1)[0]) if len(pts) > 1 else None
     if rank == 0:
         print(json.dumps({"metric": METRIC, "mode": "sweep (BASELINE config 5)", "n_gpus": world,
                           "scaling": "strong", "budget_gb_per_job": args.sweep_gb,

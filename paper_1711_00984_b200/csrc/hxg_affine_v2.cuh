@@ -54,6 +54,9 @@ struct AffCfg {
         return u;
     }
     static constexpr int NU = units();
+    // row groups per CTA: a whole element for low orders (tiny row groups), one otherwise
+    static constexpr int RG = P <= 4 ? NU : 1;
+    static constexpr int NCTA = (NU + RG - 1) / RG;  // CTAs per element
 };
 
 // Direct variant: warp w writes packed rows j1 = w, w + 4, ...; lane (kq, i1) keeps its
@@ -141,18 +144,8 @@ __global__ void __launch_bounds__(AFF2_THREADS) affine_v2_kernel(const __grid_co
     extern __shared__ __align__(16) double smem[];
     __shared__ double s_field[MAXF];
     const int tid = threadIdx.x;
-    const int u = blockIdx.x % C::NU;
-    const int e = blockIdx.x / C::NU;
-    int rem = u, b = 0;
-#pragma unroll
-    for (int bb = 0; bb < C::NB - 1; ++bb)
-        if (b == bb && rem >= C::n(bb, 1) * C::n(bb, 2)) { rem -= C::n(bb, 1) * C::n(bb, 2); b = bb + 1; }
-    int n2b = C::n(0, 1);
-#pragma unroll
-    for (int bb = 1; bb < C::NB; ++bb)
-        if (b == bb) n2b = C::n(bb, 1);
-    const int j2 = rem % n2b, j3 = rem / n2b;
-
+    const int cta = blockIdx.x % C::NCTA;
+    const int e = blockIdx.x / C::NCTA;
     double *sF = smem + C::OFF_F;
     for (int idx = tid; idx < 4 * KF * KF; idx += AFF2_THREADS) {
         const int rs = idx / (KF * KF), q = idx - rs * KF * KF, i = q / KF, j = q - i * KF;
@@ -163,41 +156,53 @@ __global__ void __launch_bounds__(AFF2_THREADS) affine_v2_kernel(const __grid_co
         dev_jacobian(args.kind[e], args.params + 24LL * e, 0.5, 0.5, 0.5, J);
         const double det = dev_metrics(J, D, Cm);
         dev_fields(S, det, D, Cm, 1.0, args.coef ? args.coef[e] : 1.0, s_field);
-        if (u == 0) {
+        if (cta == 0) {
             if (!(det > 0.0)) atomicOr(args.status + e, 1);
             if (args.kind[e] > 2) atomicOr(args.status + e, 2);  // gram.py:170-174
         }
     }
-    __syncthreads();
-    // Bs_h[a][K = (i2, i3)] for every test block a >= b
-    if constexpr (C::NB == 1) {
-        aff_bsum<S, P, 0, 0>(smem, s_field, j2, j3);
-    } else {
-        if (b == 0) {
-            aff_bsum<S, P, 0, 0>(smem, s_field, j2, j3);
-            aff_bsum<S, P, 1, 0>(smem, s_field, j2, j3);
-            aff_bsum<S, P, 2, 0>(smem, s_field, j2, j3);
-        } else if (b == 1) {
-            aff_bsum<S, P, 1, 1>(smem, s_field, j2, j3);
-            aff_bsum<S, P, 2, 1>(smem, s_field, j2, j3);
-        } else {
-            aff_bsum<S, P, 2, 2>(smem, s_field, j2, j3);
-        }
-    }
-    __syncthreads();
     double *__restrict__ outE = args.out + (long long)e * args.P;
-    if constexpr (C::NB == 1) {
-        aff_rows<S, P, 0, 0>(smem, outE, j2, j3);
-    } else {
-        if (b == 0) {
-            aff_rows<S, P, 0, 0>(smem, outE, j2, j3);
-            aff_rows<S, P, 1, 0>(smem, outE, j2, j3);
-            aff_rows<S, P, 2, 0>(smem, outE, j2, j3);
-        } else if (b == 1) {
-            aff_rows<S, P, 1, 1>(smem, outE, j2, j3);
-            aff_rows<S, P, 2, 1>(smem, outE, j2, j3);
+    const int u1 = cmin(C::NU, (cta + 1) * C::RG);
+    for (int u = cta * C::RG; u < u1; ++u) {
+        int rem = u, b = 0;
+#pragma unroll
+        for (int bb = 0; bb < C::NB - 1; ++bb)
+            if (b == bb && rem >= C::n(bb, 1) * C::n(bb, 2)) { rem -= C::n(bb, 1) * C::n(bb, 2); b = bb + 1; }
+        int n2b = C::n(0, 1);
+#pragma unroll
+        for (int bb = 1; bb < C::NB; ++bb)
+            if (b == bb) n2b = C::n(bb, 1);
+        const int j2 = rem % n2b, j3 = rem / n2b;
+        __syncthreads();  // fields / F ready; previous row group done with the Bs sums
+        // Bs_h[a][K = (i2, i3)] for every test block a >= b
+        if constexpr (C::NB == 1) {
+            aff_bsum<S, P, 0, 0>(smem, s_field, j2, j3);
         } else {
-            aff_rows<S, P, 2, 2>(smem, outE, j2, j3);
+            if (b == 0) {
+                aff_bsum<S, P, 0, 0>(smem, s_field, j2, j3);
+                aff_bsum<S, P, 1, 0>(smem, s_field, j2, j3);
+                aff_bsum<S, P, 2, 0>(smem, s_field, j2, j3);
+            } else if (b == 1) {
+                aff_bsum<S, P, 1, 1>(smem, s_field, j2, j3);
+                aff_bsum<S, P, 2, 1>(smem, s_field, j2, j3);
+            } else {
+                aff_bsum<S, P, 2, 2>(smem, s_field, j2, j3);
+            }
+        }
+        __syncthreads();
+        if constexpr (C::NB == 1) {
+            aff_rows<S, P, 0, 0>(smem, outE, j2, j3);
+        } else {
+            if (b == 0) {
+                aff_rows<S, P, 0, 0>(smem, outE, j2, j3);
+                aff_rows<S, P, 1, 0>(smem, outE, j2, j3);
+                aff_rows<S, P, 2, 0>(smem, outE, j2, j3);
+            } else if (b == 1) {
+                aff_rows<S, P, 1, 1>(smem, outE, j2, j3);
+                aff_rows<S, P, 2, 1>(smem, outE, j2, j3);
+            } else {
+                aff_rows<S, P, 2, 2>(smem, outE, j2, j3);
+            }
         }
     }
 }

@@ -426,6 +426,33 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
         return HXG_OK;
     }
 
+    // general path, low isotropic orders: one fused kernel (geometry evaluated in
+    // the contraction kernel, no metric pass / workspace)
+    {
+        const char *fg = getenv("HXG_FORCE_GENERIC"), *f2 = getenv("HXG_FORCE_V2");
+        if (p1 == p2 && p2 == p3 && p1 <= 3 && L == p1 + 1 && !(fg && fg[0] == '1') &&
+            !(f2 && f2[0] == '1')) {
+            V2Args a;
+            a.tables = tables;
+            a.metric = nullptr;
+            a.out = out;
+            a.P = Pk;
+            a.E = E;
+            a.kind = kind;
+            a.params = params;
+            a.coef = coef;
+            a.wgrid = wgrid;
+            a.status = status;
+            int r = 1;
+            switch (space) {
+            case H1: r = launch_v2_H1(p1, a, st); break;
+            case HCURL: r = launch_v2_hcurl(p1, a, st); break;
+            case HDIV: r = launch_v2_hdiv(p1, a, st); break;
+            case L2: r = launch_v2_l2(p1, a, st); break;
+            }
+            if (r <= 0) return r == 0 ? HXG_OK : HXG_ERR_CUDA;
+        }
+    }
     // general path: metric kernel then the three-stage contraction, per chunk
     if (!workspace) return HXG_ERR_WORKSPACE;
     const int Ech = elements_per_chunk(P, L, E, workspace_bytes);

@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // Specialized general-map kernels for space L2, isotropic orders p = 1..10, L = p + 1.
 #include "hxg_general_v2.cuh"
@@ -25,6 +26,9 @@ static int launch_one(const V2Args &a, int grid, cudaStream_t st)
             b.out = a.out;
             b.P = a.P;
             b.E = a.E;
+            b.kind = nullptr;
+            b.params = b.coef = b.wgrid = nullptr;
+            b.status = nullptr;
             const int want = 148 * C4::MINB * 4;
             b.split = a.E >= want ? 1 : (want + a.E - 1) / a.E;
             if (b.split > 32) b.split = 32;
@@ -34,7 +38,10 @@ static int launch_one(const V2Args &a, int grid, cudaStream_t st)
     }
     using C3 = V3Cfg<L2, P, P + 1>;
     if constexpr (C3::OK) {
-        if (!(getenv("HXG_FORCE_V2") && getenv("HXG_FORCE_V2")[0] == '1')) {
+        // fused kernels (p <= 3) evaluate the geometry themselves: they take the
+        // fused call (metric == NULL); a call with a metric array runs v2
+        if (!(getenv("HXG_FORCE_V2") && getenv("HXG_FORCE_V2")[0] == '1') &&
+            (C3::FUSED == (a.metric == nullptr))) {
             auto k3 = general_v3_kernel<L2, P, P + 1>;
             if (cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM_BYTES) != cudaSuccess)
                 return -5;
@@ -44,11 +51,19 @@ static int launch_one(const V2Args &a, int grid, cudaStream_t st)
             b.out = a.out;
             b.P = a.P;
             b.E = a.E;
+            b.kind = a.kind;
+            b.params = a.params;
+            b.coef = a.coef;
+            b.wgrid = a.wgrid;
+            b.status = a.status;
             const int want = 148 * C3::MINB * 2;
             b.split = a.E >= want ? 1 : (want + a.E - 1) / a.E;
             if (b.split > 16) b.split = 16;
             if (getenv("HXG_V3_SPLIT")) b.split = atoi(getenv("HXG_V3_SPLIT"));
-            k3<<<a.E * b.split, V3_THREADS, C3::SMEM_BYTES, st>>>(b);
+            // persistent CTAs (grid-stride over (element, part) items)
+            const long long items = (long long)a.E * b.split;
+            const int grid = (int)std::min<long long>(items, 148LL * C3::MINB * 2);
+            k3<<<grid, V3_THREADS, C3::SMEM_BYTES, st>>>(b);
             return cudaGetLastError() == cudaSuccess ? 0 : -5;
         }
     }
@@ -85,7 +100,7 @@ static int launch_aff_one(const AffV2Args &a, cudaStream_t st)
     auto k = affine_v2_kernel<L2, P>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
         return -5;
-    const long long grid = (long long)a.E * C::NU;
+    const long long grid = (long long)a.E * C::NCTA;
     if (grid >= (1ll << 31)) return -6;
     k<<<(int)grid, AFF2_THREADS, C::SMEM_BYTES, st>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : -5;

@@ -28,6 +28,10 @@ struct V2Args {
     double *out;           // [E][P]
     long long P;
     int E;
+    // inputs of the fused low-order path (metric == NULL): see V3Cfg::FUSED
+    const int *kind = nullptr;
+    const double *params = nullptr, *coef = nullptr, *wgrid = nullptr;
+    int *status = nullptr;
 };
 
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }

@@ -17,6 +17,7 @@
 // counter (dynamic balancing; the element's metric stays L1/L2-resident).
 #pragma once
 #include "hxg_common.cuh"
+#include "hxg_geom.cuh"
 #include "hxg_general_v2.cuh"
 #include "hxg_terms.h"
 
@@ -60,7 +61,11 @@ struct V3Cfg {
     static constexpr int W_TOT = W_S + 2 * C2::N1 * SW;  // [2][N1][SW] staging
     static constexpr int OFF_T = 0;                     // CTA-shared [2][KT][LP]
     static constexpr int OFF_W = 2 * KT * LP;
-    static constexpr int SMEM_BYTES = (OFF_W + V3_WARPS * W_TOT) * 8 + 16;
+    // p <= 3: the element's metric fields are evaluated in the kernel into shared
+    // memory (the separate metric pass would move as many bytes as the output)
+    static constexpr bool FUSED = P <= 3;
+    static constexpr int OFF_M = OFF_W + V3_WARPS * W_TOT;
+    static constexpr int SMEM_BYTES = (OFF_M + (FUSED ? NF * L3 : 0)) * 8 + 16;
     __host__ __device__ static constexpr int pair_units(int a, int b)
     {
         return a == b ? n(a, 2) * (n(a, 2) + 1) / 2 : n(a, 2) * n(b, 2);
@@ -83,12 +88,24 @@ struct V3Cfg {
 
 struct V3Args {
     const double *tables;
-    const double *metric;  // [E][nfields][n][l][m]
+    const double *metric;  // [E][nfields][n][l][m]; NULL for the fused low-order path
     double *out;
     long long P;
     int E;
     int split;  // CTAs per element
+    // fused low-order path (C::FUSED): geometry evaluated in the kernel
+    const int *kind;
+    const double *params, *coef, *wgrid;
+    int *status;
 };
+
+// metric field load: shared memory on the fused path, read-only global otherwise
+template <bool FUSED>
+__device__ __forceinline__ double metric_ld(const double *p)
+{
+    if constexpr (FUSED) return *p;
+    else return __ldg(p);
+}
 
 // stage-B groups listed per h: gl[h][q] = q-th g with g_h[g] == h, or -1
 struct GList {
@@ -160,7 +177,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
             for (int q = 0; q < NPASS; ++q) {
                 const int lm = cmin(lane + 32 * q, L * L - 1);
 #pragma unroll
-                for (int n = 0; n < L; ++n) v[q][n] = __ldg(Mf + n * L * L + lm);
+                for (int n = 0; n < L; ++n) v[q][n] = metric_ld<C::FUSED>(Mf + n * L * L + lm);
             }
 #pragma unroll
             for (int q = 0; q < NPASS; ++q) {
@@ -403,6 +420,100 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
 #endif
 }
 
+// Low orders (p <= 2): the same unit loop with stages B and C on DFMA.  With
+// digit extents <= 4 an 8x8 DMMA tile would be mostly padding, so each lane
+// evaluates whole B_h values and whole Gram entries and stores the entries
+// directly (consecutive lanes -> consecutive packed columns of one row).
+template <int S, int P, int L, int A, int B>
+__device__ __forceinline__ void v3s_unit(const double *sT, double *W, const double *__restrict__ M,
+                                         double *__restrict__ outE, int j3, int i3)
+{
+    using C = V3Cfg<S, P, L>;
+    constexpr CPair pp = make_pair_plan(S, A, B);
+    constexpr int LP = C::LP, L3 = C::L3, N = C::N;
+    constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1);
+    constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1);
+    constexpr int sha0 = sh_of(S, A, 0), sha1 = sh_of(S, A, 1), sha2 = sh_of(S, A, 2);
+    constexpr int shb0 = sh_of(S, B, 0), shb1 = sh_of(S, B, 1), shb2 = sh_of(S, B, 2);
+    constexpr int offA = V2Cfg<S, P, L>::off(A), offB = V2Cfg<S, P, L>::off(B);
+    const int lane = threadIdx.x & 31;
+    double *sP = W + C::W_P, *sA = W + C::W_A, *sBw = W + C::W_B;
+    auto T = [&](int f, int k, int l) { return sT[(f * KT + k) * LP + l]; };
+
+    // stage A (xi3): Abar_g[m][l]
+    for (int o = lane; o < pp.nt * 8; o += 32) {
+        const int t = o >> 3, n = o & 7;
+        int fr = 0, fs = 0;
+#pragma unroll
+        for (int tt = 0; tt < pp.nt; ++tt)
+            if (tt == t) { fr = pp.t_fr[tt]; fs = pp.t_fs[tt]; }
+        sP[o] = n < L ? T(fr, i3 + sha2, n) * T(fs, j3 + shb2, n) : 0.0;
+    }
+    __syncwarp();
+    if (lane < L * L) {
+        const int l = lane / L, m = lane - l * L;
+#pragma unroll
+        for (int g = 0; g < pp.ng; ++g) {
+            double acc = 0.0;
+#pragma unroll
+            for (int t = 0; t < pp.nt; ++t) {
+                if (pp.t_g[t] != g) continue;
+                const double *Mf = M + pp.t_field[t] * L3 + lane;
+                double s = 0.0;
+#pragma unroll
+                for (int n = 0; n < L; ++n) s = fma(metric_ld<C::FUSED>(Mf + n * L * L), sP[t * 8 + n], s);
+                acc += pp.t_sign[t] > 0 ? s : -s;
+            }
+            sA[(g * 8 + m) * 8 + l] = acc;
+        }
+    }
+    __syncwarp();
+    const int I0 = offA + n1a * n2a * i3;
+    for (int j2 = 0; j2 < n2b; ++j2) {
+        // stage B (xi2): B_h[i2][l]
+        for (int o = lane; o < n2a * L; o += 32) {
+            const int i2 = o / L, l = o - i2 * L;
+            double acc[MAXH] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int g = 0; g < pp.ng; ++g) {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < L; ++m)
+                    s = fma(T(pp.g_fr[g], i2 + sha1, m) * T(pp.g_fs[g], j2 + shb1, m), sA[(g * 8 + m) * 8 + l], s);
+                acc[pp.g_h[g]] += s;
+            }
+#pragma unroll
+            for (int h = 0; h < pp.nh; ++h) sBw[(h * 8 + i2) * 8 + l] = acc[h];
+        }
+        __syncwarp();
+        // stage C (xi1): entries of rows J = (j1, j2, j3, b), columns (i1, i2, i3, a)
+        for (int o = lane; o < n1b * n2a * n1a; o += 32) {
+            const int j1 = o / (n2a * n1a), r = o - j1 * (n2a * n1a);
+            const int i2 = r / n1a, i1 = r - i2 * n1a;
+            const int J = offB + j1 + n1b * (j2 + n2b * j3);
+            const int I = I0 + r;
+            if (I < J) continue;
+            double v = 0.0;
+#pragma unroll
+            for (int h = 0; h < pp.nh; ++h)
+#pragma unroll
+                for (int l = 0; l < L; ++l)
+                    v = fma(T(pp.h_fs[h], j1 + shb0, l) * T(pp.h_fr[h], i1 + sha0, l), sBw[(h * 8 + i2) * 8 + l], v);
+            __stcs(outE + (J * N - J * (J - 1) / 2 + (I - J)), v);
+        }
+        __syncwarp();
+    }
+}
+
+template <int S, int P, int L, int A, int B>
+__device__ __forceinline__ void v3_pick(const V3Args &args, const double *sT, double *W,
+                                        const double *__restrict__ M, double *__restrict__ outE,
+                                        int epar, int j3, int i3, int &buf, unsigned &keep)
+{
+    if constexpr (P <= 2) v3s_unit<S, P, L, A, B>(sT, W, M, outE, j3, i3);
+    else v3_unit<S, P, L, A, B>(args, sT, W, M, outE, epar, j3, i3, buf, keep);
+}
+
 template <int S, int P, int L>
 __global__ void __launch_bounds__(V3_THREADS, (V3Cfg<S, P, L>::MINB))
     general_v3_kernel(const __grid_constant__ V3Args args)
@@ -410,8 +521,6 @@ __global__ void __launch_bounds__(V3_THREADS, (V3Cfg<S, P, L>::MINB))
     using C = V3Cfg<S, P, L>;
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_next;
-    const int e = blockIdx.x / args.split;
-    const int part = blockIdx.x - e * args.split;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double *sT = smem + C::OFF_T;
     for (int idx = threadIdx.x; idx < 2 * KT * C::LP; idx += V3_THREADS) {
@@ -420,15 +529,42 @@ __global__ void __launch_bounds__(V3_THREADS, (V3Cfg<S, P, L>::MINB))
     }
     double *W = smem + C::OFF_W + warp * C::W_TOT;
     for (int idx = lane; idx < C::W_TOT; idx += 32) W[idx] = 0.0;  // zero padding of Abar/B_h
+    int buf = 0;
+    unsigned keep = 0;  // see dmma_8x8x4_keep
+    // persistent CTAs: work items (element, part) strided over the grid
+    for (long long item = blockIdx.x; item < (long long)args.E * args.split; item += gridDim.x) {
+    const int e = (int)(item / args.split);
+    const int part = (int)(item - (long long)e * args.split);
+    __syncthreads();  // previous item: every warp has left its unit loop
     if (threadIdx.x == 0) s_next = 0;
+    const double *M;
+    if constexpr (C::FUSED) {  // metric fields of this element (metric_kernel's body)
+        double *sM = smem + C::OFF_M;
+        const double *par = args.params + 24LL * e;
+        const int knd = args.kind[e];
+        const double cf = args.coef ? args.coef[e] : 1.0;
+        for (int pt = threadIdx.x; pt < C::L3; pt += V3_THREADS) {
+            const int n = pt / (L * L), l = (pt / L) % L, m = pt % L;
+            double J[3][3], D[6], Cm[6], f[MAXF];
+            dev_jacobian(knd, par, args.tables[TAB_NODES + l], args.tables[TAB_NODES + m],
+                         args.tables[TAB_NODES + n], J);
+            const double det = dev_metrics(J, D, Cm);
+            const double w = args.tables[TAB_WTS + l] * args.tables[TAB_WTS + m] * args.tables[TAB_WTS + n];
+            const double c = args.wgrid ? args.wgrid[(long long)e * C::L3 + (l * L + m) * L + n] : cf;
+            dev_fields(S, det, D, Cm, w, c, f);
+#pragma unroll
+            for (int k = 0; k < C::NF; ++k) sM[k * C::L3 + pt] = f[k];
+            if (!(det > 0.0) && part == 0) atomicOr(args.status + e, 1);
+        }
+        M = sM;
+    } else {
+        M = args.metric + (long long)e * C::NF * C::L3;
+    }
     __syncthreads();
-    const double *__restrict__ M = args.metric + (long long)e * C::NF * C::L3;
     double *__restrict__ outE = args.out + (long long)e * args.P;
     const int epar = (int)((reinterpret_cast<size_t>(outE) >> 3) & 1);
     const int lo = (int)((long long)C::NU * part / args.split);
     const int hi = (int)((long long)C::NU * (part + 1) / args.split);
-    int buf = 0;
-    unsigned keep = 0;  // see dmma_8x8x4_keep
     for (;;) {
         int u = 0;
         if (lane == 0) u = atomicAdd(&s_next, 1);
@@ -460,18 +596,19 @@ __global__ void __launch_bounds__(V3_THREADS, (V3Cfg<S, P, L>::MINB))
                 }
             }
         if constexpr (C::NB == 1) {
-            v3_unit<S, P, L, 0, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep);
+            v3_pick<S, P, L, 0, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep);
         } else {
             switch (pair) {
-            case 0: v3_unit<S, P, L, 0, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
-            case 3: v3_unit<S, P, L, 1, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
-            case 6: v3_unit<S, P, L, 2, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
-            case 4: v3_unit<S, P, L, 1, 1>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
-            case 7: v3_unit<S, P, L, 2, 1>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
-            default: v3_unit<S, P, L, 2, 2>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 0: v3_pick<S, P, L, 0, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 3: v3_pick<S, P, L, 1, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 6: v3_pick<S, P, L, 2, 0>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 4: v3_pick<S, P, L, 1, 1>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            case 7: v3_pick<S, P, L, 2, 1>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
+            default: v3_pick<S, P, L, 2, 2>(args, sT, W, M, outE, epar, j3, i3, buf, keep); break;
             }
         }
     }
+    }  // item loop
     if (args.E < 0 && keep == 0x9e3779b9u) args.out[0] = keep;  // never taken; keeps `keep` live
     bulk_wait_all();
 }
