@@ -24,6 +24,7 @@ struct AffV2Args {
     int *status;
     long long P;
     int E;
+    int rg;  // row groups per CTA (host: whole elements only for low orders and large batches)
 };
 
 template <int S, int P>
@@ -54,9 +55,7 @@ struct AffCfg {
         return u;
     }
     static constexpr int NU = units();
-    // row groups per CTA: a whole element for low orders (tiny row groups), one otherwise
-    static constexpr int RG = P <= 4 ? NU : 1;
-    static constexpr int NCTA = (NU + RG - 1) / RG;  // CTAs per element
+
 };
 
 // Direct variant: warp w writes packed rows j1 = w, w + 4, ...; lane (kq, i1) keeps its
@@ -144,8 +143,9 @@ __global__ void __launch_bounds__(AFF2_THREADS) affine_v2_kernel(const __grid_co
     extern __shared__ __align__(16) double smem[];
     __shared__ double s_field[MAXF];
     const int tid = threadIdx.x;
-    const int cta = blockIdx.x % C::NCTA;
-    const int e = blockIdx.x / C::NCTA;
+    const int ncta = (C::NU + args.rg - 1) / args.rg;  // CTAs per element
+    const int cta = blockIdx.x % ncta;
+    const int e = blockIdx.x / ncta;
     double *sF = smem + C::OFF_F;
     for (int idx = tid; idx < 4 * KF * KF; idx += AFF2_THREADS) {
         const int rs = idx / (KF * KF), q = idx - rs * KF * KF, i = q / KF, j = q - i * KF;
@@ -162,8 +162,8 @@ __global__ void __launch_bounds__(AFF2_THREADS) affine_v2_kernel(const __grid_co
         }
     }
     double *__restrict__ outE = args.out + (long long)e * args.P;
-    const int u1 = cmin(C::NU, (cta + 1) * C::RG);
-    for (int u = cta * C::RG; u < u1; ++u) {
+    const int u1 = cmin(C::NU, (cta + 1) * args.rg);
+    for (int u = cta * args.rg; u < u1; ++u) {
         int rem = u, b = 0;
 #pragma unroll
         for (int bb = 0; bb < C::NB - 1; ++bb)
