@@ -87,7 +87,7 @@ class ClockSampler:
             self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.tmp, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -313,8 +313,18 @@ def measure_device(wl, E, lo, steps, warmup, world, device, with_clocks=True):
         dist.barrier()
     torch.cuda.synchronize(device)
     sampler = ClockSampler(device.index if device.index is not None else 0) if with_clocks else None
+
+    def keep_busy(seconds):
+        # untimed steps around the timed region so the ~20 ms nvidia-smi samples
+        # see the clocks of the loaded GPU even when the timed region is short
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            ds.step(stream)
+            torch.cuda.synchronize(device)
+
     if sampler:
         sampler.__enter__()
+        keep_busy(0.3)
     for k in range(steps):
         ds.flush()  # L2 flush between timed iterations (outside the timed events)
         ev[k][0].record(stream)
@@ -322,6 +332,7 @@ def measure_device(wl, E, lo, steps, warmup, world, device, with_clocks=True):
         ev[k][2].record(stream)
     torch.cuda.synchronize(device)
     if sampler:
+        keep_busy(0.3)
         sampler.__exit__(None, None, None)
     if world > 1:
         import torch.distributed as dist
