@@ -15,7 +15,7 @@ static int launch_one(const V2Args &a, int grid, cudaStream_t st)
     using C4 = V4Cfg<H1, P, P + 1>;
     if constexpr (C4::OK && P >= 5) {
         const char *v4env = getenv("HXG_USE_V4");
-        const bool use_v4 = P >= 8 || (v4env && v4env[0] == '1');
+        const bool use_v4 = v4env && v4env[0] == '1';  // opt-in: v2 measures faster at p >= 8
         if (use_v4 && !(getenv("HXG_FORCE_V2") && getenv("HXG_FORCE_V2")[0] == '1')) {
             auto k4 = general_v4_kernel<H1, P, P + 1>;
             if (cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, C4::SMEM_BYTES) != cudaSuccess)
