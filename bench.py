@@ -251,16 +251,20 @@ class DeviceStep:
         self.out = torch.empty((E, self.P), dtype=torch.float64, device=dev)
         self.status = torch.zeros(E, dtype=torch.int32, device=dev)
         self.tab = self.eng.tables(self.L)
+        # p <= 3 runs one fused kernel (geometry in the contraction kernel): time the
+        # whole hxg_gram_batched call; otherwise time metric and contraction separately,
+        # with a workspace holding the metric fields of the whole batch
+        # (hxg_workspace_size is capped at one 512 MB launch chunk)
+        self.fused = wl.path == "general" and wl.p <= 3
         ws = self.lib.hxg_workspace_size(self.sc, 0 if wl.path == "general" else 1,
                                          *wl.orders, self.L, E)
+        per = self.lib.hxg_workspace_size(self.sc, 0, *wl.orders, self.L, 1) if wl.path == "general" else 0
+        self.full_metric = wl.path == "general" and not self.fused and E * per <= (16 << 30)
+        if self.full_metric:
+            ws = E * per
         self.ws_bytes = ws
         self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
-        # p <= 3 runs one fused kernel (geometry in the contraction kernel): time the
-        # whole hxg_gram_batched call; otherwise time metric and contraction separately
-        self.fused = wl.path == "general" and wl.p <= 3
-        self.full_metric = (not self.fused) and (
-            ws >= self.lib.hxg_workspace_size(self.sc, 0, *wl.orders, self.L, E)
-            if wl.path == "general" else True)
+        self.chunks = -(-E // max(1, ws // per)) if per else 1
         self.flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
         self.launches_per_step = 0
 
@@ -292,7 +296,7 @@ class DeviceStep:
         assert rc == 0, rc
         if ev_mid is not None and wl.path == "general":
             ev_mid.record(stream)
-        self.launches_per_step = 1 if wl.path == "affine" else 2
+        self.launches_per_step = 1 if wl.path == "affine" else (1 if self.fused else 2 * self.chunks)
 
 
 def measure_device(wl, E, lo, steps, warmup, world, device, with_clocks=True):

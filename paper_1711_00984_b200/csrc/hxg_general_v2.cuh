@@ -34,6 +34,10 @@ struct V2Args {
     int *status = nullptr;
 };
 
+#ifndef HXG_V2_STAGEB_EFF
+#define HXG_V2_STAGEB_EFF 0.5
+#endif
+
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 
@@ -109,6 +113,13 @@ struct V2Cfg {
     static constexpr int NU = units();
     static constexpr int MINB = SMEM_BYTES <= 113 * 1024 ? 2 : 1;
 
+    // stage B on DMMA when the 8x8x4 tiles are not mostly padding: columns l pad to
+    // 8, the contraction over m pads to 4 (rows run over the flattened (j2, i2) index)
+    __host__ __device__ static constexpr bool stageb_dmma()
+    {
+        return (double)L / (8 * ((L + 7) / 8)) * (double)L / (4 * ((L + 3) / 4)) >= HXG_V2_STAGEB_EFF;
+    }
+
     // stage-C factorization per block pair (see file header)
     __host__ __device__ static constexpr int yq(int a, int b)  // max #h sharing one test function
     {
@@ -134,16 +145,39 @@ struct V2Cfg {
 __device__ __forceinline__ void st_cs(double *p, double v) { __stcs(p, v); }
 
 // bulk (TMA-engine) copy shared -> global, 16-byte aligned, size multiple of 16
+// The Gram output is written once and never re-read by the kernel: mark it
+// evict-first in L2 so the stream does not push the (re-read) metric fields
+// out to DRAM.
+#ifndef HXG_BULK_HINT
+#define HXG_BULK_HINT 1
+#endif
 __device__ __forceinline__ void bulk_s2g(double *gdst, const double *ssrc, int bytes)
 {
     const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+#if HXG_BULK_HINT
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(gdst),
+                 "r"(s), "r"(bytes), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s), "r"(bytes)
                  : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// timing-only switches (wrong results): bit 0 skips stage A, 1 stage B, 2 the
+// stage-C DMMAs, 3 the bulk write-out
+#ifndef HXG_V2_SKIP
+#define HXG_V2_SKIP 0
+#endif
+#ifndef HXG_V2_STAGEB_DMMA
+#define HXG_V2_STAGEB_DMMA 1
+#endif
 
 template <int S, int P, int L, int A, int B>
 __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int e, int j3)
@@ -233,9 +267,10 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
         const int ncols = n1a * n2a * r3;
         __syncthreads();
         // ---------------- stage A: contract xi3 -> Abar_g[ii3][g][m][l] ----------------
-#pragma unroll
-        for (int g = 0; g < pp.ng; ++g) {
-            for (int it = tid; it < r3 * L * L; it += GEN_THREADS) {
+        // (g, ii3, l, m) items over all threads (the group index is a runtime value)
+        for (int it2 = tid; it2 < (HXG_V2_SKIP & 1 ? 0 : pp.ng * r3 * L * L); it2 += GEN_THREADS) {
+            const int g = it2 / (r3 * L * L), it = it2 - g * (r3 * L * L);
+            {
                 const int ii3 = it / (L * L), lm = it - ii3 * (L * L);
                 const int i3 = i3lo + ii3;
                 double acc = 0.0;
@@ -258,9 +293,56 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
             const int r2 = cmin(R2, n2b - j2lo);
             __syncthreads();
             // ---------------- stage B: contract xi2 -> B_h[jj2][h][ii3][i2][l] ----------------
+#if HXG_V2_STAGEB_DMMA
+            // on DMMA: B_h[(jj2,i2)][l] = sum_{g in h} sum_m V_g[(jj2,i2)][m] Abar_g[m][l] with
+            // V_g = u_fr(i2,m) u_fs(j2,m); tile rows run over the flattened (jj2, i2) index,
+            // one warp per (h, ii3, 8-row tile), all l tiles in flight
+            if constexpr (C::stageb_dmma()) {
+                constexpr int NLT = (L + 7) / 8, LQ = (L + 3) / 4;
+                const int nrt = (r2 * n2a + 7) >> 3;
+                for (int w = warp; w < (HXG_V2_SKIP & 2 ? 0 : pp.nh * r3 * nrt); w += GEN_WARPS) {
+                    const int h = w / (r3 * nrt), w2 = w - h * (r3 * nrt);
+                    const int ii3 = w2 / nrt, rt = w2 - ii3 * nrt;
+                    const int row = rt * 8 + g8;
+                    const bool rv = row < r2 * n2a;
+                    const int jj2 = rv ? row / n2a : 0, i2 = rv ? row - jj2 * n2a : 0;
+                    const int j2 = j2lo + jj2;
+                    double d[NLT][2];
 #pragma unroll
-            for (int h = 0; h < pp.nh; ++h) {
-                for (int it = tid; it < R2 * R3 * n2a; it += GEN_THREADS) {
+                    for (int lt = 0; lt < NLT; ++lt) d[lt][0] = d[lt][1] = 0.0;
+#pragma unroll
+                    for (int g = 0; g < pp.ng; ++g) {
+                        if (pp.g_h[g] != h) continue;
+                        const double *Ta = sT + (pp.g_fr[g] * KT + i2 + sha1) * LP;
+                        const double *Tb = sT + (pp.g_fs[g] * KT + j2 + shb1) * LP;
+                        const double *Ag = sA + (ii3 * NG + g) * L * LP;
+#pragma unroll
+                        for (int ks = 0; ks < LQ; ++ks) {
+                            const int m = ks * 4 + t4;
+                            const double av = (m < L && rv) ? Ta[m] * Tb[m] : 0.0;
+#pragma unroll
+                            for (int lt = 0; lt < NLT; ++lt) {
+                                const double bv = m < L ? Ag[m * LP + lt * 8 + g8] : 0.0;
+                                dmma_8x8x4(d[lt][0], d[lt][1], av, bv);
+                            }
+                        }
+                    }
+                    if (rv) {
+                        double *dst = sB + jj2 * SJ2 + ((h * R3 + ii3) * N2 + i2) * LP;
+#pragma unroll
+                        for (int lt = 0; lt < NLT; ++lt) {
+                            const int l = lt * 8 + 2 * t4;
+                            if (l < L) dst[l] = d[lt][0];
+                            if (l + 1 < L) dst[l + 1] = d[lt][1];
+                        }
+                    }
+                }
+            } else
+#endif
+            // (h, jj2, ii3, i2) items over all threads
+            for (int it2 = tid; it2 < (HXG_V2_SKIP & 2 ? 0 : pp.nh * R2 * R3 * n2a); it2 += GEN_THREADS) {
+                const int h = it2 / (R2 * R3 * n2a), it = it2 - h * (R2 * R3 * n2a);
+                {
                     const int i2 = it % n2a, q = it / n2a, ii3 = q % R3, jj2 = q / R3;
                     if (ii3 >= r3 || jj2 >= r2) continue;
                     const int j2 = j2lo + jj2;
@@ -333,7 +415,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
 #pragma unroll
                     for (int mt = 0; mt < NMT; ++mt) d[mt][0] = d[mt][1] = 0.0;
 #pragma unroll
-                    for (int ks = 0; ks < NKS; ++ks) {
+                    for (int ks = 0; ks < (HXG_V2_SKIP & 4 ? 0 : NKS); ++ks) {
                         const double bv = X[ks] * sBj[bo[ks]];
 #pragma unroll
                         for (int mt = 0; mt < NMT; ++mt) dmma_8x8x4(d[mt][0], d[mt][1], Af[mt][ks], bv);
@@ -380,6 +462,20 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
             fence_proxy_async();  // staging writes -> visible to the bulk-copy (async) proxy
             __syncthreads();
             // ---------------- write-out: one bulk copy per packed row segment ----------------
+#ifdef HXG_V2_NO_BULK
+            {  // warp per row, coalesced 8-byte stores (staging free at the next barrier)
+                const int rows = r2 * n1b;
+                for (int row = warp; row < rows; row += GEN_WARPS) {
+                    const int jj2 = row / n1b, j1 = row - jj2 * n1b;
+                    const int goff = row_goff(jj2, j1);
+                    const int J = offB + j1 + n1b * (j2lo + jj2 + n2b * j3);
+                    const int cs = J > I0 ? J - I0 : 0;
+                    const double *src = sS + row * SLD + ((epar + goff) & 1);
+                    for (int c = cs + lane; c < ncols; c += 32) st_cs(outE + goff + c, src[c]);
+                }
+            }
+            if (false)
+#endif
             {
                 const int rows = r2 * n1b;
                 for (int row = tid; row < rows; row += GEN_THREADS) {
@@ -399,7 +495,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                         --len;
                     }
                     if (len & 1) st_cs(dst + len - 1, src[len - 1]);  // 8-byte tail
-                    if (len >= 2) bulk_s2g(dst, src, (len & ~1) * 8);
+                    if (len >= 2 && !(HXG_V2_SKIP & 8)) bulk_s2g(dst, src, (len & ~1) * 8);
                 }
                 bulk_commit();
             }
