@@ -80,7 +80,7 @@ struct V2Cfg {
     __host__ __device__ static constexpr int sld(int R3) { return ((C12 * R3 + 7) / 8) * 8 + 2; }
     __host__ __device__ static constexpr int smem(int R2, int R3)
     {
-        return 2 * KT * LP + R3 * NG * L * LP + R2 * NH * R3 * N2 * LP + R2 * N1 * sld(R3);
+        return 2 * KT * LP + R3 * NG * L * LP + R2 * NH * R3 * N2 * LP + R2 * N1 * sld(R3) + (R2 * N1 + 1) / 2;
     }
     __host__ __device__ static constexpr int pick_r3()
     {
@@ -101,6 +101,7 @@ struct V2Cfg {
     static constexpr int OFF_A = OFF_T + 2 * KT * LP;
     static constexpr int OFF_B = OFF_A + R3 * NG * L * LP;
     static constexpr int OFF_S = OFF_B + R2 * NH * R3 * N2 * LP;
+    static constexpr int OFF_R = OFF_S + R2 * N1 * SLD;  // int[R2 * N1]: staging row offsets
     static constexpr int SMEM_BYTES = smem(R2, R3) * 8;
     static constexpr int SJ2 = NH * R3 * N2 * LP;  // sB stride per j2
     static constexpr int SH = R3 * N2 * LP;        // sB stride per h
@@ -199,6 +200,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
     double *sA = smem + C::OFF_A;
     double *sB = smem + C::OFF_B;
     double *sS = smem + C::OFF_S;
+    int *sRow = reinterpret_cast<int *>(smem + C::OFF_R);
     const double *__restrict__ M = args.metric + (long long)e * C::NF * L3;
     double *__restrict__ outE = args.out + (long long)e * args.P;
 
@@ -372,9 +374,6 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                     for (int l2 = 0; l2 < LP / 2; ++l2) dst[l2] = make_double2(acc[2 * l2], acc[2 * l2 + 1]);
                 }
             }
-            bulk_wait_read();  // previous chunk's bulk stores have read the staging buffer
-            __syncthreads();
-            // ---------------- stage C: contract xi1 on DMMA ----------------
             // staging row `row` = (jj2, j1) is shifted by pad(row) in {0,1} doubles so that
             // it has the 16-byte phase of its global destination (bulk-copy alignment)
             const int I0 = offA + n1a * n2a * i3lo;
@@ -382,6 +381,13 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 const int J = offB + j1 + n1b * (j2lo + jj2 + n2b * j3);
                 return J * N - J * (J - 1) / 2 - J + I0;  // &G(J, I0) - outE
             };
+            for (int row = tid; row < r2 * n1b; row += GEN_THREADS) {
+                const int jj2 = row / n1b, j1 = row - jj2 * n1b;
+                sRow[row] = row * SLD + ((epar + row_goff(jj2, j1)) & 1);
+            }
+            bulk_wait_read();  // previous chunk's bulk stores have read the staging buffer
+            __syncthreads();
+            // ---------------- stage C: contract xi1 on DMMA ----------------
             if constexpr (!YF) {
                 const int nct = (ncols + 7) >> 3;
                 const int T = nct * r2;
@@ -390,8 +396,8 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 int ct = -1;
                 double X[NKS];
                 int bo[NKS];
+                int ctn = it0 / r2, jj2 = it0 - ctn * r2;  // tiles (ct, jj2), jj2 fastest
                 for (int it = it0; it < it1; ++it) {
-                    const int ctn = it / r2, jj2 = it - ctn * r2;
                     if (ctn != ct) {
                         ct = ctn;
                         const int c = ct * 8 + g8;
@@ -424,11 +430,14 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                     for (int mt = 0; mt < NMT; ++mt) {
                         const int j1 = mt * 8 + g8;
                         if (j1 < n1b) {
-                            const int pad = (epar + row_goff(jj2, j1)) & 1;
-                            double *dst = sS + (jj2 * n1b + j1) * SLD + pad + ct * 8 + 2 * t4;
+                            double *dst = sS + sRow[jj2 * n1b + j1] + ct * 8 + 2 * t4;
                             dst[0] = d[mt][0];
                             dst[1] = d[mt][1];
                         }
+                    }
+                    if (++jj2 == r2) {
+                        jj2 = 0;
+                        ++ctn;
                     }
                 }
             } else {
@@ -448,8 +457,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                         dmma_8x8x4(d0, d1, y, Yb[ks]);
                     }
                     if (g8 < n1b) {
-                        const int pad = (epar + row_goff(jj2, g8)) & 1;
-                        double *dst = sS + (jj2 * n1b + g8) * SLD + pad + (ii3 * n2a + i2) * n1a + 2 * t4;
+                        double *dst = sS + sRow[jj2 * n1b + g8] + (ii3 * n2a + i2) * n1a + 2 * t4;
                         if (2 * t4 < n1a) dst[0] = d0;
                         if (2 * t4 + 1 < n1a) dst[1] = d1;
                     }
