@@ -14,8 +14,14 @@
 //           A operand = trial 1D table (registers), B operand = table x B_h
 //   Y-form: D[j1, i1] (per (i2,i3)) = sum_{r,l} Y_r[j1,l] u_r(i1,l),
 //           Y_r[j1,l] = sum_{h: r(h)=r} u_s(h)(j1,l) B_h[l]  (built per fragment)
+//   P-form: D[(j2,i3,i2), (j1,i1)] = sum_{h,l} B_h[j2,i3,i2,l] * (u_s(j1,l) u_r(i1,l))
+//           rows and columns both flattened: no digit padding of the 8x8 tiles,
+//           B operand in registers, scattered staging stores (B-form pads j1 to
+//           a multiple of 8: 56-69% tile occupancy at digit extents 9-11)
 // The Y-form needs about nr*L FMAs per Gram entry instead of nh*L (H1: 2L vs
 // 4L), at the price of 8x8 output tiles that span only n1a x n1b entries.
+// Stage B (contraction over xi2) runs on DMMA as well when its tiles are dense
+// enough (stageb_dmma), on DFMA otherwise.
 #pragma once
 #include "hxg_common.cuh"
 #include "hxg_terms.h"
@@ -179,6 +185,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef HXG_V2_STAGEB_DMMA
 #define HXG_V2_STAGEB_DMMA 1
 #endif
+#ifndef HXG_V2_PFORM
+#define HXG_V2_PFORM 1
+#endif
 
 template <int S, int P, int L, int A, int B>
 __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int e, int j3)
@@ -193,6 +202,9 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
     constexpr int shb0 = sh_of(S, B, 0), shb1 = sh_of(S, B, 1), shb2 = sh_of(S, B, 2);
     constexpr int offA = C::off(A), offB = C::off(B);
     constexpr bool YF = C::yform(A, B);
+    // product form instead of the B-form when the contraction is long enough (nh >= 3:
+    // H1, H(curl)) to amortize its scattered staging stores; measured on p = 8..10
+    constexpr bool PF = !YF && HXG_V2_PFORM && pp.nh >= 3;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;
@@ -210,14 +222,15 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
     constexpr int NMT = (n1b + 7) / 8;         // B-form row tiles
     constexpr int YQ = C::yq(A, B);            // Y-form trial factors per test function
     constexpr int KSY = (pp.nr * L + 3) / 4;   // Y-form k-steps (segments may straddle)
-    constexpr int NKR = YF ? 1 : NKS;          // register array extents
+    constexpr int NKR = (YF || PF) ? 1 : NKS;  // register array extents
     constexpr int NYR = YF ? KSY : 1;
     double Af[NMT][NKR];
     double Yb[NYR];
     double Yc[NYR][YQ];
     int Yo[NYR][YQ];
     (void)Af; (void)Yb; (void)Yc; (void)Yo;
-    if constexpr (!YF) {
+    if constexpr (PF) {
+    } else if constexpr (!YF) {
 #pragma unroll
         for (int mt = 0; mt < NMT; ++mt)
 #pragma unroll
@@ -388,7 +401,74 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
             bulk_wait_read();  // previous chunk's bulk stores have read the staging buffer
             __syncthreads();
             // ---------------- stage C: contract xi1 on DMMA ----------------
-            if constexpr (!YF) {
+            if constexpr (PF) {
+                // product form: G[(jj2,ii3,i2), (j1,i1)] = sum_{h,l} B_h[jj2][ii3][i2][l] * [u_s(j1,l) u_r(i1,l)]
+                // Tile rows (jj2, ii3, i2) and columns (j1, i1) are both flattened, so the
+                // 8x8 tiles carry no digit padding (the B-form pads j1 to 8 or 16).  The B
+                // operand (a product of two 1D tables) stays in registers while a warp
+                // sweeps the row tiles of one column tile, two row tiles in flight.
+                constexpr int NCOL = n1b * n1a, NCT = (NCOL + 7) / 8;
+                const int nrow = r2 * r3 * n2a, nrt = (nrow + 7) >> 3;
+                const int nrtp = (nrt + 1) >> 1;  // row-tile pairs per column tile
+                const int T = NCT * nrtp;
+                const int per = (T + GEN_WARPS - 1) / GEN_WARPS;
+                const int it0 = warp * per, it1 = cmin(T, it0 + per);
+                double Bp[NKS];
+                int ko[NKS];
+                int ctc = -1, dj1[2] = {0, 0}, di1[2] = {0, 0};
+                for (int it = it0; it < it1; ++it) {
+                    const int ct = it / nrtp, rt0 = 2 * (it - ct * nrtp);
+                    if (ct != ctc) {  // (re)load the B fragment of column tile ct
+                        ctc = ct;
+                        const int col = ct * 8 + g8;
+                        const bool cv = col < NCOL;
+                        const int j1 = cv ? col / n1a : 0, i1 = cv ? col - (col / n1a) * n1a : 0;
+#pragma unroll
+                        for (int ks = 0; ks < NKS; ++ks) {
+                            const int k = ks * 4 + t4;
+                            const int h = k / L, l = k - h * L;
+                            int fs = 0, fr = 0;
+#pragma unroll
+                            for (int hh = 0; hh < pp.nh; ++hh)
+                                if (hh == h) { fs = pp.h_fs[hh]; fr = pp.h_fr[hh]; }
+                            const bool v = k < KD;
+                            Bp[ks] = (v && cv) ? sT[(fs * KT + j1 + shb0) * LP + l] * sT[(fr * KT + i1 + sha0) * LP + l]
+                                               : 0.0;
+                            ko[ks] = v ? h * SH + l : 0;
+                        }
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) {  // output columns 2 t4 + e2 of this lane
+                            const int oc = ct * 8 + 2 * t4 + e2;
+                            dj1[e2] = oc < NCOL ? oc / n1a : -1;
+                            di1[e2] = oc - (oc / n1a) * n1a;
+                        }
+                    }
+                    double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                    int ao[2], jr[2], sc[2];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {  // this lane's row g8 of row tile rt0 + c
+                        const int row = (rt0 + c) * 8 + g8;
+                        const bool rv = row < nrow;
+                        const int i2 = rv ? row % n2a : 0, q = rv ? row / n2a : 0;
+                        const int ii3 = R3 == 1 ? 0 : q % r3, jj2 = R3 == 1 ? q : q / r3;
+                        ao[c] = rv ? jj2 * SJ2 + (ii3 * N2 + i2) * LP : 0;
+                        jr[c] = rv ? jj2 * n1b : -1;
+                        sc[c] = (ii3 * n2a + i2) * n1a;
+                    }
+#pragma unroll
+                    for (int ks = 0; ks < (HXG_V2_SKIP & 4 ? 0 : NKS); ++ks) {
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) dmma_8x8x4(d[c][0], d[c][1], sB[ao[c] + ko[ks]], Bp[ks]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        if (jr[c] < 0) continue;
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2)
+                            if (dj1[e2] >= 0) sS[sRow[jr[c] + dj1[e2]] + sc[c] + di1[e2]] = d[c][e2];
+                    }
+                }
+            } else if constexpr (!YF) {
                 const int nct = (ncols + 7) >> 3;
                 const int T = nct * r2;
                 const int per = (T + GEN_WARPS - 1) / GEN_WARPS;
