@@ -26,10 +26,10 @@ namespace hxg {
 #ifndef HXG_V3_DEBUG_EMIN
 #define HXG_V3_DEBUG_EMIN 0
 #endif
-#ifndef HXG_V3_I2_UNROLL
-#define HXG_V3_I2_UNROLL 8
+#ifndef HXG_V3_TF
+#define HXG_V3_TF 4
 #endif
-constexpr int kI2Unroll = HXG_V3_I2_UNROLL;
+constexpr int kTF = HXG_V3_TF;  // stage-C output tiles in flight per warp
 #if defined(HXG_V3_DEBUG) || defined(HXG_V3_DEBUG2)
 __device__ double *hxg_dbg;
 #endif
@@ -81,8 +81,8 @@ struct V3Cfg {
 #ifdef HXG_V3_MINB
     static constexpr int MINB = HXG_V3_MINB;
 #else
-    // CTAs per SM: 5 (<= 102 registers) measured best for H1/H(curl)/H(div), 4 for L2
-    static constexpr int MINB = cmin(S == L2 ? 4 : 5, (228 * 1024) / (SMEM_BYTES + 1024));
+    // CTAs per SM: 5 (<= 102 registers) measured best for H1/H(curl), 4 for H(div) and L2
+    static constexpr int MINB = cmin((S == L2 || S == HDIV) ? 4 : 5, (228 * 1024) / (SMEM_BYTES + 1024));
 #endif
 };
 
@@ -314,12 +314,14 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
         // ---------------- stage C: contract xi1 on DMMA ----------------
         if constexpr (YF) {
 #pragma unroll
-            for (int i2 = 0; i2 < n2a; i2 += 2) {  // two tiles (i2, i2 + 1) in flight
-                double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            for (int i2 = 0; i2 < n2a; i2 += kTF) {  // kTF tiles (i2, i2 + 1, ...) in flight
+                double d[kTF][2];
+#pragma unroll
+                for (int c = 0; c < kTF; ++c) d[c][0] = d[c][1] = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < KSY; ++ks) {
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
+                    for (int c = 0; c < kTF; ++c) {
                         if (i2 + c < n2a) {
                             const double *base = sBw + (i2 + c) * 8;
                             double y = Yc[ks][0] * base[Ro[ks][0]];
@@ -330,7 +332,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
                     }
                 }
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
+                for (int c = 0; c < kTF; ++c)
                     if (i2 + c < n2a && g8 < n1b) {
                         if (2 * t4 < n1a) srow[(i2 + c) * n1a + 2 * t4] = d[c][0];
                         if (2 * t4 + 1 < n1a) srow[(i2 + c) * n1a + 2 * t4 + 1] = d[c][1];
@@ -338,18 +340,20 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
             }
         } else {
 #pragma unroll
-            for (int i1 = 0; i1 < n1a; i1 += 2) {  // two tiles (i1, i1 + 1) in flight
-                double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            for (int i1 = 0; i1 < n1a; i1 += kTF) {  // kTF tiles (i1, i1 + 1, ...) in flight
+                double d[kTF][2];
+#pragma unroll
+                for (int c = 0; c < kTF; ++c) d[c][0] = d[c][1] = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < NKS; ++ks) {
                     const double bb = sBw[Ro[ks][0]];
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
+                    for (int c = 0; c < kTF; ++c)
                         if (i1 + c < n1a)
                             dmma_8x8x4_keep(d[c][0], d[c][1], R0[ks], sT[Xo[ks] + (i1 + c) * LP] * bb, keep);
                 }
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
+                for (int c = 0; c < kTF; ++c)
                     if (i1 + c < n1a && g8 < n1b) {  // columns i2 = 2 t4, 2 t4 + 1
                         if (2 * t4 < n2a) srow[(2 * t4) * n1a + i1 + c] = d[c][0];
                         if (2 * t4 + 1 < n2a) srow[(2 * t4 + 1) * n1a + i1 + c] = d[c][1];
@@ -386,6 +390,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
                 if (len & 1) __stcs(dst + len - 1, src[len - 1]);
 #ifdef HXG_V3_NO_BULK
                 for (int c = 0; c < (len & ~1); ++c) __stcs(dst + c, src[c]);
+#elif defined(HXG_V3_SKIP_W)  // timing experiment only: no bulk write-out
 #else
                 if (len >= 2) bulk_s2g(dst, src, (len & ~1) * 8);
 #endif
@@ -558,7 +563,11 @@ __global__ void __launch_bounds__(V3_THREADS, (V3Cfg<S, P, L>::MINB))
         }
         M = sM;
     } else {
+#ifdef HXG_V3_FAKE_M  // timing experiment only: every element reads element 0's metric
+        M = args.metric;
+#else
         M = args.metric + (long long)e * C::NF * C::L3;
+#endif
     }
     __syncthreads();
     double *__restrict__ outE = args.out + (long long)e * args.P;
