@@ -71,7 +71,7 @@ static int launch_one(const V2Args &a, int grid, cudaStream_t st)
     auto k = general_v2_kernel<HCURL, P, P + 1>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
         return -5;
-    k<<<grid, GEN_THREADS, C::SMEM_BYTES, st>>>(a);
+    k<<<grid, V2_THREADS, C::SMEM_BYTES, st>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 

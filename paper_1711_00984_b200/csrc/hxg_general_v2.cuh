@@ -40,6 +40,15 @@ struct V2Args {
     int *status = nullptr;
 };
 
+#ifndef HXG_V2_WARPS
+#define HXG_V2_WARPS 8
+#endif
+#ifndef HXG_V2_BUDGET_KB
+#define HXG_V2_BUDGET_KB 110
+#endif
+constexpr int V2_WARPS = HXG_V2_WARPS;
+constexpr int V2_THREADS = V2_WARPS * 32;
+
 #ifndef HXG_V2_STAGEB_EFF
 #define HXG_V2_STAGEB_EFF 0.5
 #endif
@@ -82,7 +91,7 @@ struct V2Cfg {
         return m;
     }
     static constexpr int NG = maxg(), NH = maxh();
-    static constexpr int BUDGET = (110 * 1024) / 8;  // doubles: 2 CTAs per SM
+    static constexpr int BUDGET = (HXG_V2_BUDGET_KB * 1024) / 8;  // doubles (110 KB: 2 CTAs per SM)
     __host__ __device__ static constexpr int sld(int R3) { return ((C12 * R3 + 7) / 8) * 8 + 2; }
     __host__ __device__ static constexpr int smem(int R2, int R3)
     {
@@ -188,6 +197,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef HXG_V2_PFORM
 #define HXG_V2_PFORM 1
 #endif
+#ifndef HXG_V2_PF_MINNH
+#define HXG_V2_PF_MINNH 3
+#endif
 
 template <int S, int P, int L, int A, int B>
 __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int e, int j3)
@@ -204,7 +216,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
     constexpr bool YF = C::yform(A, B);
     // product form instead of the B-form when the contraction is long enough (nh >= 3:
     // H1, H(curl)) to amortize its scattered staging stores; measured on p = 8..10
-    constexpr bool PF = !YF && HXG_V2_PFORM && pp.nh >= 3;
+    constexpr bool PF = !YF && HXG_V2_PFORM && pp.nh >= HXG_V2_PF_MINNH;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;
@@ -283,7 +295,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
         __syncthreads();
         // ---------------- stage A: contract xi3 -> Abar_g[ii3][g][m][l] ----------------
         // (g, ii3, l, m) items over all threads (the group index is a runtime value)
-        for (int it2 = tid; it2 < (HXG_V2_SKIP & 1 ? 0 : pp.ng * r3 * L * L); it2 += GEN_THREADS) {
+        for (int it2 = tid; it2 < (HXG_V2_SKIP & 1 ? 0 : pp.ng * r3 * L * L); it2 += V2_THREADS) {
             const int g = it2 / (r3 * L * L), it = it2 - g * (r3 * L * L);
             {
                 const int ii3 = it / (L * L), lm = it - ii3 * (L * L);
@@ -315,7 +327,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
             if constexpr (C::stageb_dmma()) {
                 constexpr int NLT = (L + 7) / 8, LQ = (L + 3) / 4;
                 const int nrt = (r2 * n2a + 7) >> 3;
-                for (int w = warp; w < (HXG_V2_SKIP & 2 ? 0 : pp.nh * r3 * nrt); w += GEN_WARPS) {
+                for (int w = warp; w < (HXG_V2_SKIP & 2 ? 0 : pp.nh * r3 * nrt); w += V2_WARPS) {
                     const int h = w / (r3 * nrt), w2 = w - h * (r3 * nrt);
                     const int ii3 = w2 / nrt, rt = w2 - ii3 * nrt;
                     const int row = rt * 8 + g8;
@@ -355,7 +367,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
             } else
 #endif
             // (h, jj2, ii3, i2) items over all threads
-            for (int it2 = tid; it2 < (HXG_V2_SKIP & 2 ? 0 : pp.nh * R2 * R3 * n2a); it2 += GEN_THREADS) {
+            for (int it2 = tid; it2 < (HXG_V2_SKIP & 2 ? 0 : pp.nh * R2 * R3 * n2a); it2 += V2_THREADS) {
                 const int h = it2 / (R2 * R3 * n2a), it = it2 - h * (R2 * R3 * n2a);
                 {
                     const int i2 = it % n2a, q = it / n2a, ii3 = q % R3, jj2 = q / R3;
@@ -394,7 +406,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 const int J = offB + j1 + n1b * (j2lo + jj2 + n2b * j3);
                 return J * N - J * (J - 1) / 2 - J + I0;  // &G(J, I0) - outE
             };
-            for (int row = tid; row < r2 * n1b; row += GEN_THREADS) {
+            for (int row = tid; row < r2 * n1b; row += V2_THREADS) {
                 const int jj2 = row / n1b, j1 = row - jj2 * n1b;
                 sRow[row] = row * SLD + ((epar + row_goff(jj2, j1)) & 1);
             }
@@ -407,22 +419,24 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 // 8x8 tiles carry no digit padding (the B-form pads j1 to 8 or 16).  The B
                 // operand (a product of two 1D tables) stays in registers while a warp
                 // sweeps the row tiles of one column tile, two row tiles in flight.
-                constexpr int NCOL = n1b * n1a, NCT = (NCOL + 7) / 8;
+                // columns (j1, i1) with i1 padded to an even count, so a lane's two output
+                // columns (2 t4, 2 t4 + 1) share j1 and sit next to each other in staging
+                constexpr int N1E = (n1a + 1) & ~1, NCOL = n1b * N1E, NCT = (NCOL + 7) / 8;
                 const int nrow = r2 * r3 * n2a, nrt = (nrow + 7) >> 3;
                 const int nrtp = (nrt + 1) >> 1;  // row-tile pairs per column tile
                 const int T = NCT * nrtp;
-                const int per = (T + GEN_WARPS - 1) / GEN_WARPS;
+                const int per = (T + V2_WARPS - 1) / V2_WARPS;
                 const int it0 = warp * per, it1 = cmin(T, it0 + per);
                 double Bp[NKS];
                 int ko[NKS];
-                int ctc = -1, dj1[2] = {0, 0}, di1[2] = {0, 0};
+                int ctc = -1, dj1 = -1, di1 = 0;
                 for (int it = it0; it < it1; ++it) {
                     const int ct = it / nrtp, rt0 = 2 * (it - ct * nrtp);
                     if (ct != ctc) {  // (re)load the B fragment of column tile ct
                         ctc = ct;
                         const int col = ct * 8 + g8;
-                        const bool cv = col < NCOL;
-                        const int j1 = cv ? col / n1a : 0, i1 = cv ? col - (col / n1a) * n1a : 0;
+                        const int j1 = col / N1E, i1 = col - j1 * N1E;
+                        const bool cv = col < NCOL && i1 < n1a;
 #pragma unroll
                         for (int ks = 0; ks < NKS; ++ks) {
                             const int k = ks * 4 + t4;
@@ -436,11 +450,10 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                                                : 0.0;
                             ko[ks] = v ? h * SH + l : 0;
                         }
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {  // output columns 2 t4 + e2 of this lane
-                            const int oc = ct * 8 + 2 * t4 + e2;
-                            dj1[e2] = oc < NCOL ? oc / n1a : -1;
-                            di1[e2] = oc - (oc / n1a) * n1a;
+                        {  // output columns 2 t4, 2 t4 + 1 of this lane
+                            const int oc = ct * 8 + 2 * t4;
+                            dj1 = oc < NCOL ? oc / N1E : -1;
+                            di1 = oc - (oc / N1E) * N1E;
                         }
                     }
                     double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -460,18 +473,20 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
 #pragma unroll
                         for (int c = 0; c < 2; ++c) dmma_8x8x4(d[c][0], d[c][1], sB[ao[c] + ko[ks]], Bp[ks]);
                     }
+                    if (dj1 >= 0 && !(HXG_V2_SKIP & 16)) {
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        if (jr[c] < 0) continue;
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2)
-                            if (dj1[e2] >= 0) sS[sRow[jr[c] + dj1[e2]] + sc[c] + di1[e2]] = d[c][e2];
+                        for (int c = 0; c < 2; ++c) {
+                            if (jr[c] < 0) continue;
+                            double *dst = sS + sRow[jr[c] + dj1] + sc[c] + di1;
+                            dst[0] = d[c][0];
+                            if (di1 + 1 < n1a) dst[1] = d[c][1];
+                        }
                     }
                 }
             } else if constexpr (!YF) {
                 const int nct = (ncols + 7) >> 3;
                 const int T = nct * r2;
-                const int per = (T + GEN_WARPS - 1) / GEN_WARPS;
+                const int per = (T + V2_WARPS - 1) / V2_WARPS;
                 const int it0 = warp * per, it1 = cmin(T, it0 + per);
                 int ct = -1;
                 double X[NKS];
@@ -522,7 +537,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 }
             } else {
                 const int T = r3 * n2a * r2;  // tiles (ii3, i2, jj2), jj2 fastest
-                const int per = (T + GEN_WARPS - 1) / GEN_WARPS;
+                const int per = (T + V2_WARPS - 1) / V2_WARPS;
                 const int it0 = warp * per, it1 = cmin(T, it0 + per);
                 int qd = it0 / r2, jj2 = it0 - qd * r2;
                 int ii3 = qd / n2a, i2 = qd - ii3 * n2a;
@@ -553,7 +568,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
 #ifdef HXG_V2_NO_BULK
             {  // warp per row, coalesced 8-byte stores (staging free at the next barrier)
                 const int rows = r2 * n1b;
-                for (int row = warp; row < rows; row += GEN_WARPS) {
+                for (int row = warp; row < rows; row += V2_WARPS) {
                     const int jj2 = row / n1b, j1 = row - jj2 * n1b;
                     const int goff = row_goff(jj2, j1);
                     const int J = offB + j1 + n1b * (j2lo + jj2 + n2b * j3);
@@ -566,7 +581,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
 #endif
             {
                 const int rows = r2 * n1b;
-                for (int row = tid; row < rows; row += GEN_THREADS) {
+                for (int row = tid; row < rows; row += V2_THREADS) {
                     const int jj2 = row / n1b, j1 = row - jj2 * n1b;
                     const int goff = row_goff(jj2, j1);
                     const int J = offB + j1 + n1b * (j2lo + jj2 + n2b * j3);
@@ -593,7 +608,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
 }
 
 template <int S, int P, int L>
-__global__ void __launch_bounds__(GEN_THREADS, (V2Cfg<S, P, L>::MINB))
+__global__ void __launch_bounds__(V2_THREADS, (V2Cfg<S, P, L>::MINB))
     general_v2_kernel(const __grid_constant__ V2Args args)
 {
     using C = V2Cfg<S, P, L>;
@@ -612,7 +627,7 @@ __global__ void __launch_bounds__(GEN_THREADS, (V2Cfg<S, P, L>::MINB))
             }
         }
     double *sT = smem + C::OFF_T;
-    for (int idx = threadIdx.x; idx < 2 * KT * C::LP; idx += GEN_THREADS) {
+    for (int idx = threadIdx.x; idx < 2 * KT * C::LP; idx += V2_THREADS) {
         const int fk = idx / C::LP, l = idx - fk * C::LP;
         sT[idx] = l < L ? args.tables[TAB_T + fk * LT + l] : 0.0;
     }
