@@ -8,6 +8,7 @@
 // packed rows J = (j1, j2, j3, b): the Bs sums go to shared memory, then each
 // warp streams whole packed rows to HBM with coalesced stores (aff_rows).
 #pragma once
+#include <cstdlib>
 #include "hxg_common.cuh"
 #include "hxg_general_v2.cuh"
 #include "hxg_geom.cuh"
@@ -24,8 +25,25 @@ struct AffV2Args {
     int *status;
     long long P;
     int E;
-    int rg;  // row groups per CTA (host: whole elements only for low orders and large batches)
+    int rg;  // row groups per CTA (aff_row_groups)
 };
+
+// Row groups per CTA: about 128 KB of output per CTA (per-CTA setup and tail
+// effects dominate tiny row groups; whole elements for small elements), one
+// group per CTA once a group alone carries >= 32 KB, and at least ~16 CTAs per
+// SM.  Measured (profiles/affine_rg_r01.txt) on H1 p3-p10, H(curl) p4-p10,
+// H(div) p5/p7.
+inline int aff_row_groups(int NU, long long P, int E)
+{
+    long long target = 128LL << 10;
+    if (const char *t = getenv("HXG_AFF_TARGET_KB")) target = 1024LL * atoll(t);  // tuning
+    const double per_group = 8.0 * (double)P / NU;  // mean output bytes of one row group
+    long long rg = per_group >= 32768.0 ? 1 : (long long)(target / per_group);
+    rg = rg < 1 ? 1 : (rg > NU ? NU : rg);
+    while (rg > 1 && (long long)E * ((NU + rg - 1) / rg) < 148LL * 16) rg = (rg + 1) / 2;
+    if (const char *r = getenv("HXG_AFF_RG")) rg = atoi(r) < 1 ? 1 : (atoi(r) > NU ? NU : atoi(r));  // tuning
+    return (int)rg;
+}
 
 template <int S, int P>
 struct AffCfg {

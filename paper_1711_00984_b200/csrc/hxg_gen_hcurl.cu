@@ -103,7 +103,7 @@ static int launch_aff_one(const AffV2Args &a, cudaStream_t st)
     // low orders with many elements: one CTA per element (row groups are tiny);
     // otherwise one CTA per packed row group
     AffV2Args b = a;
-    b.rg = (P <= 4 && (long long)a.E * C::NU >= 148LL * 64) ? C::NU : 1;
+    b.rg = aff_row_groups(C::NU, a.P, a.E);
     const long long grid = (long long)a.E * ((C::NU + b.rg - 1) / b.rg);
     if (grid >= (1ll << 31)) return -6;
     k<<<(int)grid, AFF2_THREADS, C::SMEM_BYTES, st>>>(b);
