@@ -276,3 +276,28 @@ def test_specialized_equals_generic(space, p, monkeypatch):
     for got in (spec, spec4, spec2):
         rel = torch.linalg.norm(got - gen, dim=1) / torch.linalg.norm(gen, dim=1)
         assert float(rel.max()) <= TOL
+
+
+@pytest.mark.parametrize("space", SPACES)
+@pytest.mark.parametrize("p", [1, 3, 5, 6, 8])
+def test_affine_row_group_split_invariant(space, p, monkeypatch, orc):
+    """The constant-Jacobian kernel gives bit-identical packed rows whether a CTA
+    owns one row group, a few, or the whole element (HXG_AFF_RG overrides the
+    size-based choice of aff_row_groups), and matches the oracle."""
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import affine_batch
+
+    b = affine_batch(5, 900 + p, variable_coef=True)
+    outs = []
+    for rg in ("1", "3", "1000"):
+        monkeypatch.setenv("HXG_AFF_RG", rg)
+        got, st = gram_batched(space, (p, p, p), b.kind, b.params, b.coef, path="affine")
+        torch.cuda.synchronize()
+        assert int(st.abs().sum()) == 0
+        outs.append(got.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    ref = orc.gram_batched(space, "affine", (p, p, p), 1, b.kind, b.params, b.coef)
+    rel = np.linalg.norm(outs[0] - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert rel.max() <= TOL
