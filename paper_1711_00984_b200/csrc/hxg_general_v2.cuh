@@ -197,6 +197,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef HXG_V2_PFORM
 #define HXG_V2_PFORM 1
 #endif
+#ifndef HXG_V2_AREG
+#define HXG_V2_AREG 1
+#endif
 #ifndef HXG_V2_PF_MINNH
 #define HXG_V2_PF_MINNH 3
 #endif
@@ -288,12 +291,48 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
     }
     const int epar = (int)((reinterpret_cast<size_t>(outE) >> 3) & 1);
 
+    // Stage A with the metric in registers: when every group is one term and one
+    // pass of the CTA covers all (g, l, m) items (H(div), L2 at p >= 8), each
+    // thread loads its L metric values once per unit instead of once per i3 (the
+    // values do not depend on i3; the reload latency sat on a CTA barrier)
+    constexpr bool AREG = R3 == 1 && pp.nt == pp.ng && pp.ng * L * L <= V2_THREADS && HXG_V2_AREG;
+    double mv[AREG ? L : 1];
+    (void)mv;
+    if constexpr (AREG) {
+        const int g = tid / (L * L), lm = tid - g * (L * L);
+        int fld = 0;
+#pragma unroll
+        for (int t = 0; t < pp.nt; ++t)
+            if (pp.t_g[t] == g) fld = pp.t_field[t];
+        const bool v = tid < pp.ng * L * L;
+#pragma unroll
+        for (int n = 0; n < L; ++n) mv[n] = v ? __ldg(M + fld * L3 + n * L * L + lm) : 0.0;
+    }
+
     const int i3first = (A == B) ? j3 : 0;
     for (int i3lo = i3first; i3lo < n3a; i3lo += R3) {
         const int r3 = cmin(R3, n3a - i3lo);
         const int ncols = n1a * n2a * r3;
         __syncthreads();
         // ---------------- stage A: contract xi3 -> Abar_g[ii3][g][m][l] ----------------
+        if constexpr (AREG) {
+            if (tid < pp.ng * L * L && !(HXG_V2_SKIP & 1)) {
+                const int g = tid / (L * L), lm = tid - g * (L * L);
+                const int i3 = i3lo;
+                double s = 0.0;
+#pragma unroll
+                for (int t = 0; t < pp.nt; ++t) {
+                    if (pp.t_g[t] != g) continue;
+                    const double *Ta = sT + (pp.t_fr[t] * KT + i3 + sha2) * LP;
+                    const double *Tb = sT + (pp.t_fs[t] * KT + j3 + shb2) * LP;
+#pragma unroll
+                    for (int n = 0; n < L; ++n) s = fma(mv[n], Ta[n] * Tb[n], s);
+                    if (pp.t_sign[t] < 0) s = -s;
+                }
+                const int l = lm / L, m = lm - l * L;
+                sA[(g * L + m) * LP + l] = s;
+            }
+        } else
         // (g, ii3, l, m) items over all threads (the group index is a runtime value)
         for (int it2 = tid; it2 < (HXG_V2_SKIP & 1 ? 0 : pp.ng * r3 * L * L); it2 += V2_THREADS) {
             const int g = it2 / (r3 * L * L), it = it2 - g * (r3 * L * L);
