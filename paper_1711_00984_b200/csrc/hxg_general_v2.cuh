@@ -197,6 +197,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef HXG_V2_PFORM
 #define HXG_V2_PFORM 1
 #endif
+#ifndef HXG_V2_EVEN_CHUNKS
+#define HXG_V2_EVEN_CHUNKS 1
+#endif
 #ifndef HXG_V2_AREG
 #define HXG_V2_AREG 1
 #endif
@@ -355,9 +358,13 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 sA[((ii3 * NG + g) * L + m) * LP + l] = acc;
             }
         }
-        for (int j2lo = 0; j2lo < n2b; j2lo += R2) {
-            const int r2 = cmin(R2, n2b - j2lo);
-            __syncthreads();
+        // j2 chunks of equal size (n2b = 11, R2 = 8 -> 6 + 5 rather than 8 + 3)
+        constexpr int NCH = (n2b + R2 - 1) / R2, R2E = HXG_V2_EVEN_CHUNKS ? (n2b + NCH - 1) / NCH : R2;
+        for (int j2lo = 0; j2lo < n2b; j2lo += R2E) {
+            const int r2 = cmin(R2E, n2b - j2lo);
+            if (j2lo == 0) __syncthreads();  // stage A (sA) complete; later chunks: the
+                                             // barrier before the write-out already orders
+                                             // stage C reads of sB before its next writes
             // ---------------- stage B: contract xi2 -> B_h[jj2][h][ii3][i2][l] ----------------
 #if HXG_V2_STAGEB_DMMA
             // on DMMA: B_h[(jj2,i2)][l] = sum_{g in h} sum_m V_g[(jj2,i2)][m] Abar_g[m][l] with
