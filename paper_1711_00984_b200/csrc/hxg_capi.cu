@@ -571,7 +571,7 @@ int hxg_expand_full(int N, int E, const double *packed, double *full, void *stre
 }
 
 // Host-buffer entry: the reference's calling convention (numpy in, numpy out).
-// Inputs are copied once; the batch is integrated in ~256 MB output chunks on two
+// Inputs are copied once; the batch is integrated in ~64 MB output chunks on two
 // streams so that the device->host copy of chunk i overlaps the integration of
 // chunk i+1.  Device buffers and streams live in a per-device context that grows
 // on demand and is reused by later calls (no cudaMalloc/cudaFree per call).
@@ -625,7 +625,9 @@ int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, in
     }
     const long long Pk = (long long)P.N * (P.N + 1) / 2;
     const size_t out_bytes_el = (size_t)Pk * sizeof(double);
-    long long ch = std::max<long long>(1, (256ll << 20) / (long long)out_bytes_el);
+    long long chunk_bytes = 64ll << 20;  // D2H granularity: small chunks overlap the copy engine sooner
+    if (const char *c = getenv("HXG_HOST_CHUNK_MB")) chunk_bytes = std::max(1ll, atoll(c)) << 20;  // tuning
+    long long ch = std::max<long long>(1, chunk_bytes / (long long)out_bytes_el);
     ch = std::min<long long>(ch, E);
     size_t ws = path == GENERAL ? hxg_workspace_size(space, path, p1, p2, p3, L, (int)ch) : 0;
     int *d_kind = (int *)cx.get(0, sizeof(int) * (size_t)E, ok);
