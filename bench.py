@@ -38,6 +38,7 @@ L2_BYTES = 126 * 2 ** 20
 PEAK_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "peaks_r01.jsonl")
 NCU_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+PATH_CODES = {"general": 0, "affine": 1, "extrusion": 2}
 
 
 def algorithmic(space, orders, path, L):
@@ -168,7 +169,7 @@ def cpu_rate(wl, seconds, nthreads=0):
 
     threads = nthreads or oracle.num_cpus()
     b = wl.batch(64)
-    L = wl.L if wl.path == "general" else 1
+    L = wl.L if wl.path != "affine" else 1
     oracle.gram_batched(wl.space, wl.path, wl.orders, L, b.kind[:threads], b.params[:threads],
                         b.coef[:threads], nthreads=threads)  # warm
     n = max(threads, 8)
@@ -193,7 +194,7 @@ def run_reference(args, wl, world, rank):
     rate, _, _, _ = cpu_rate(wl, 1.0, threads)
     per_step = max(threads, int(rate * 2.0))
     b = wl.batch(per_step)
-    L = wl.L if wl.path == "general" else 1
+    L = wl.L if wl.path != "affine" else 1
     for _ in range(args.warmup):
         oracle.gram_batched(wl.space, wl.path, wl.orders, L, b.kind, b.params, b.coef,
                             nthreads=threads)
@@ -245,7 +246,8 @@ class DeviceStep:
         self.params = torch.as_tensor(b.params).to(dev)
         self.coef = torch.as_tensor(b.coef).to(dev)
         self.sc = _native.SPACE_CODES[wl.space]
-        self.L = wl.L if wl.path == "general" else 1
+        self.L = wl.L if wl.path != "affine" else 1
+        self.pc = PATH_CODES[wl.path]
         N = dim(wl.space, wl.orders)
         self.P = N * (N + 1) // 2
         self.out = torch.empty((E, self.P), dtype=torch.float64, device=dev)
@@ -256,7 +258,7 @@ class DeviceStep:
         # with a workspace holding the metric fields of the whole batch
         # (hxg_workspace_size is capped at one 512 MB launch chunk)
         self.fused = wl.path == "general" and wl.p <= 3
-        ws = self.lib.hxg_workspace_size(self.sc, 0 if wl.path == "general" else 1,
+        ws = self.lib.hxg_workspace_size(self.sc, self.pc,
                                          *wl.orders, self.L, E)
         per = self.lib.hxg_workspace_size(self.sc, 0, *wl.orders, self.L, 1) if wl.path == "general" else 0
         self.full_metric = wl.path == "general" and not self.fused and E * per <= (16 << 30)
@@ -287,16 +289,16 @@ class DeviceStep:
             assert rc == 0, rc
             self.launches_per_step = 2
             return
-        if ev_mid is not None and wl.path == "affine":
+        if ev_mid is not None and wl.path != "general":
             ev_mid.record(stream)
-        rc = lib.hxg_gram_batched(self.sc, 0 if wl.path == "general" else 1, *wl.orders, self.L,
+        rc = lib.hxg_gram_batched(self.sc, self.pc, *wl.orders, self.L,
                                   self.E, self._p(self.kind), self._p(self.params),
                                   self._p(self.coef), None, self._p(self.tab), self._p(self.out),
                                   self._p(self.status), self._p(self.ws), self.ws_bytes, s)
         assert rc == 0, rc
         if ev_mid is not None and wl.path == "general":
             ev_mid.record(stream)
-        self.launches_per_step = 1 if wl.path == "affine" else (1 if self.fused else 2 * self.chunks)
+        self.launches_per_step = 1 if wl.path != "general" else (1 if self.fused else 2 * self.chunks)
 
 
 def measure_device(wl, E, lo, steps, warmup, world, device, with_clocks=True):
@@ -410,7 +412,8 @@ def run_ours(args, wl, world, rank, local):
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": src_hbm}
     roof.update({
-        "kernel": "general_kernel (hxg_contract_batched)" if wl.path == "general" else "affine_kernel",
+        "kernel": {"general": "general_kernel (hxg_contract_batched)", "affine": "affine_v2_kernel",
+                   "extrusion": "ext_v2_kernel"}[wl.path],
         "kernel_ms_per_launch": kmean_s * 1e3,
         "algorithmic_flops_per_launch": E * F, "algorithmic_bytes_per_launch": E * B,
         "flops_per_element": F, "bytes_per_element": B,
@@ -480,7 +483,8 @@ def run_sweep(args, world, rank, local):
 
     from paper_1711_00984_b200 import _native
     from paper_1711_00984_b200.engine import get_engine
-    from paper_1711_00984_b200.inputs import affine_batch, packed_size, trilinear_batch
+    from paper_1711_00984_b200.inputs import (affine_batch, extrusion_batch, packed_size,
+                                              trilinear_batch)
 
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
@@ -494,13 +498,13 @@ def run_sweep(args, world, rank, local):
     base_n = 4096
     results = []
     stream = torch.cuda.current_stream(device)
-    for path, maps in (("general", "trilinear"), ("affine", "affine")):
-        gen = trilinear_batch if maps == "trilinear" else affine_batch
+    for path, maps in (("general", "trilinear"), ("affine", "affine"), ("extrusion", "extrusion")):
+        gen = {"trilinear": trilinear_batch, "affine": affine_batch, "extrusion": extrusion_batch}[maps]
         base = gen(base_n, 4)  # seed 4 (config 5)
         for space in ("H1", "Hcurl", "Hdiv"):
             for p in range(2, args.sweep_pmax + 1):
                 orders = (p, p, p)
-                L = p + 1 if path == "general" else 1
+                L = p + 1 if path != "affine" else 1
                 Pk = packed_size(space, orders)
                 Eg = int(budget // (8 * Pk))
                 lo, hi = shard(Eg, world, rank)
@@ -546,7 +550,7 @@ def run_sweep(args, world, rank, local):
                                 "bound": "fp64" if F / fp64 / 1e3 > B / hbm else "hbm"})
                 del kind, params, coef, status, ws
     fits = {}
-    for path in ("general", "affine"):
+    for path in ("general", "affine", "extrusion"):
         for space in ("H1", "Hcurl", "Hdiv"):
             for pmin in (2, 5):
                 pts = [r for r in results if r["path"] == path and r["space"] == space

@@ -22,6 +22,8 @@
  *            the codes here are the library's own)
  *   path   : 0 = general map, sum factorization O(p^7)  (gram_tensorized)
  *            1 = constant-Jacobian map, O(p^6)           (gram_simplified, kinds 0..2)
+ *            2 = extrusion map, O(p^6): F tables in xi1, L x L rule in (xi2, xi3)
+ *                at xi1 = 0.5                            (gram_simplified, kinds 0..3)
  *   kind   : element-map kind codes of geometry.py:46-52
  *            (0 identity, 1 diagonal-affine, 2 general-affine, 3 extrusion, 4 trilinear)
  *   params : 24 doubles per element, layout of geometry.py:83-119
@@ -34,8 +36,9 @@
  *            (entry (r,c), r <= c, at r*N - r*(r-1)/2 + (c-r))
  *   status : [E] int bit mask, written by the call: 0 ok; bit 0: det J <= 0 at
  *            an evaluated point (the reference raises DegenerateMapError,
- *            errors.py:12-20); bit 1: constant-Jacobian path asked for a map
- *            kind > 2 (SimplificationNotApplicableError, gram.py:170-174)
+ *            errors.py:12-20); bit 1: simplified path asked for a map kind it
+ *            does not cover -- > 2 on path 1, > 3 on path 2
+ *            (SimplificationNotApplicableError, gram.py:170-174)
  *
  * All pointers of hxg_gram_batched are DEVICE pointers; the call is
  * stream-ordered, does no host synchronisation and is safe to issue from
@@ -91,8 +94,9 @@ int hxg_make_tables(int L, const double *nodes, const double *weights, double *t
 /* Device workspace (bytes) needed by hxg_gram_batched for this call. */
 size_t hxg_workspace_size(int space, int path, int p1, int p2, int p3, int L, int E);
 
-/* Batched Gram integration -- replaces tens_*_{std,alt} (path 0) and
- * simp_*_const (path 1).  tables from hxg_make_tables(L, ...). */
+/* Batched Gram integration -- replaces tens_*_{std,alt} (path 0),
+ * simp_*_const (path 1, _kernels.py:1169-1404) and simp_*_ext (path 2,
+ * _kernels.py:1405-1764).  tables from hxg_make_tables(L, ...) (path 1: any L). */
 int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E,
                      const int *kind, const double *params, const double *coef,
                      const double *wgrid, const double *tables, double *out, int *status,

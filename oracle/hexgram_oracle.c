@@ -15,8 +15,9 @@
  * Reference citations are /root/reference/pkg/src/hexgram/<file>:<line>.
  * The restatement keeps the reference's *alternative* loop order
  * (quadrature loops outermost, _kernels.py:406-454, 541-624, 742-853,
- * 1003-1150) and the simplified constant-Jacobian kernels
- * (_kernels.py:1169-1404); both loop orders of the reference produce
+ * 1003-1150), the simplified constant-Jacobian kernels
+ * (_kernels.py:1169-1404) and the simplified extrusion kernels
+ * (_kernels.py:1405-1764); both loop orders of the reference produce
  * bit-identical matrices (pkg/tests/test_gram.py:103-112).
  *
  * Output convention of the batched entry: per element, the packed upper
@@ -31,7 +32,7 @@
 #include <unistd.h>
 
 enum { ORC_H1 = 0, ORC_HCURL = 1, ORC_HDIV = 2, ORC_L2 = 3 };
-enum { ORC_GENERAL = 0, ORC_AFFINE = 1 };
+enum { ORC_GENERAL = 0, ORC_AFFINE = 1, ORC_EXTRUSION = 2 };
 
 /* ------------------------------------------------------------------ */
 /* 1D machinery                                                         */
@@ -822,6 +823,308 @@ static long long simp_hcurl(int p1, int p2, int p3, const double *fall, int nF, 
     mirror_lower(G, N);
     return acc;
 }
+
+/* ------------------------------------------------------------------ */
+/* simplified kernels, extrusion maps (_kernels.py:1405-1764):          */
+/* quadrature in (xi2, xi3) at xi1 = 0.5, F-table factor in xi1          */
+/* ------------------------------------------------------------------ */
+
+/* _kernels.py:1412-1451 (simp_l2_ext) */
+static long long simp_l2_ext(int p1, int p2, int p3, const double *fall, int nF, int L,
+                             const double *nd, const double *wt, int kind, const double *par,
+                             double wmass, double *G)
+{
+    int N = p1 * p2 * p3;
+    double nu2[64], nu3[64], J[3][3], Ji[3][3];
+    double *gB = malloc(sizeof(double) * p2 * p2);
+    long long acc = 0;
+    for (int j3 = 0; j3 < p3; ++j3)
+        for (int i3 = j3; i3 < p3; ++i3) {
+            for (int t = 0; t < p2 * p2; ++t) gB[t] = 0.0;
+            for (int m = 0; m < L; ++m) {
+                orc_shape1_l2(nd[m], p2, nu2);
+                double gA = 0.0;
+                for (int n = 0; n < L; ++n) {
+                    orc_shape1_l2(nd[n], p3, nu3);
+                    double detj = orc_geom_full(kind, par, 0.5, nd[m], nd[n], J, Ji);
+                    gA += nu3[i3] * nu3[j3] * wmass * wt[n] / detj;
+                }
+                for (int j2 = 0; j2 < p2; ++j2)
+                    for (int i2 = j2; i2 < p2; ++i2) gB[i2 * p2 + j2] += nu2[i2] * nu2[j2] * gA * wt[m];
+            }
+            for (int j2 = 0; j2 < p2; ++j2)
+                for (int i2 = j2; i2 < p2; ++i2)
+                    for (int j1 = 0; j1 < p1; ++j1)
+                        for (int i1 = j1; i1 < p1; ++i1) {
+                            int I = i1 + p1 * (i2 + p2 * i3), Jf = j1 + p1 * (j2 + p2 * j3);
+                            G[(size_t)I * N + Jf] = FT(3, i1 + 1, j1 + 1) * gB[i2 * p2 + j2];
+                            ++acc;
+                        }
+        }
+    free(gB);
+    fill_l2_sym(G, p1, p2, p3);
+    return acc;
+}
+
+/* _kernels.py:1454-1531 (simp_h1_ext) with _rs_h1 (1160-1166) */
+static long long simp_h1_ext(int p1, int p2, int p3, const double *fall, int nF, int L,
+                             const double *nd, const double *wt, int kind, const double *par,
+                             double wmass, double *G)
+{
+    int q1 = p1 + 1, q2 = p2 + 1, q3 = p3 + 1, N = q1 * q2 * q3;
+    double chi2[64], dchi2[64], chi3[64], dchi3[64], J[3][3], Ji[3][3], D[3][3], gA[3][3];
+    double *gBbar = malloc(sizeof(double) * q2 * q2);
+    double *gB = malloc(sizeof(double) * 9 * q2 * q2);
+#define GB(a, b, i, j) gB[(((a) * 3 + (b)) * q2 + (i)) * q2 + (j)]
+    long long acc = 0;
+    for (int j3 = 0; j3 < q3; ++j3)
+        for (int i3 = j3; i3 < q3; ++i3) {
+            for (int t = 0; t < q2 * q2; ++t) gBbar[t] = 0.0;
+            for (int t = 0; t < 9 * q2 * q2; ++t) gB[t] = 0.0;
+            for (int m = 0; m < L; ++m) {
+                orc_shape1_h1(nd[m], p2, chi2, dchi2);
+                double gAbar = 0.0;
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) gA[a][b] = 0.0;
+                for (int n = 0; n < L; ++n) {
+                    orc_shape1_h1(nd[n], p3, chi3, dchi3);
+                    double detj = orc_geom_full(kind, par, 0.5, nd[m], nd[n], J, Ji);
+                    metric_d(Ji, D);
+                    double wq = wt[n] * detj;
+                    gAbar += chi3[i3] * chi3[j3] * wmass * wq;
+                    for (int a = 0; a < 3; ++a) {
+                        double fa = a == 2 ? dchi3[i3] : chi3[i3];
+                        for (int b = 0; b < 3; ++b) {
+                            double fb = b == 2 ? dchi3[j3] : chi3[j3];
+                            gA[a][b] += fa * fb * D[a][b] * wq;
+                        }
+                    }
+                }
+                for (int j2 = 0; j2 < q2; ++j2)
+                    for (int i2 = 0; i2 < q2; ++i2) {
+                        gBbar[i2 * q2 + j2] += chi2[i2] * chi2[j2] * gAbar * wt[m];
+                        for (int a = 0; a < 3; ++a) {
+                            double fa = a == 1 ? dchi2[i2] : chi2[i2];
+                            for (int b = 0; b < 3; ++b) {
+                                double fb = b == 1 ? dchi2[j2] : chi2[j2];
+                                GB(a, b, i2, j2) += fa * fb * gA[a][b] * wt[m];
+                            }
+                        }
+                    }
+            }
+            for (int j2 = 0; j2 < q2; ++j2)
+                for (int i2 = 0; i2 < q2; ++i2)
+                    for (int j1 = 0; j1 < q1; ++j1)
+                        for (int i1 = 0; i1 < q1; ++i1) {
+                            int I = i1 + q1 * (i2 + q2 * i3), Jf = j1 + q1 * (j2 + q2 * j3);
+                            if (I < Jf) continue;
+                            double val = FT(0, i1, j1) * gBbar[i2 * q2 + j2];
+                            ++acc;
+                            for (int a = 0; a < 3; ++a)
+                                for (int b = 0; b < 3; ++b) {
+                                    int rs = 2 * (a == 0) + (b == 0);
+                                    val += FT(rs, i1, j1) * GB(a, b, i2, j2);
+                                    ++acc;
+                                }
+                            G[(size_t)I * N + Jf] += val;
+                        }
+        }
+#undef GB
+    free(gBbar);
+    free(gB);
+    mirror_lower(G, N);
+    return acc;
+}
+
+/* _kernels.py:1534-1637 (simp_hdiv_ext) */
+static long long simp_hdiv_ext(int p1, int p2, int p3, const double *fall, int nF, int L,
+                               const double *nd, const double *wt, int kind, const double *par,
+                               double wmass, double *G)
+{
+    int q1 = p1 + 1, q2 = p2 + 1, q3 = p3 + 1, N = orc_dim(ORC_HDIV, p1, p2, p3);
+    double chi2[64], dchi2[64], chi3[64], dchi3[64], J[3][3], Ji[3][3], C[3][3];
+    double gA[3][3], gAt[3][3];
+    double *gB = malloc(sizeof(double) * 9 * q2 * q2);
+    double *gBt = malloc(sizeof(double) * 9 * q2 * q2);
+#define GB(x, a, b, i, j) x[(((a) * 3 + (b)) * q2 + (i)) * q2 + (j)]
+    long long acc = 0;
+    for (int j3 = 0; j3 < q3; ++j3)
+        for (int i3 = 0; i3 < q3; ++i3) {
+            for (int t = 0; t < 9 * q2 * q2; ++t) gB[t] = gBt[t] = 0.0;
+            for (int m = 0; m < L; ++m) {
+                orc_shape1_h1(nd[m], p2, chi2, dchi2);
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) gA[a][b] = gAt[a][b] = 0.0;
+                for (int n = 0; n < L; ++n) {
+                    orc_shape1_h1(nd[n], p3, chi3, dchi3);
+                    double detj = orc_geom_full(kind, par, 0.5, nd[m], nd[n], J, Ji);
+                    metric_c(J, C);
+                    double wq = wt[n] / detj;
+                    double wm = wmass * wq;
+                    for (int a = 0; a < 3; ++a) {
+                        int ia3 = a == 2 ? i3 : i3 + 1;
+                        if (ia3 > p3) continue;
+                        double fa = a == 2 ? chi3[ia3] : dchi3[ia3];
+                        for (int b = 0; b < 3; ++b) {
+                            int jb3 = b == 2 ? j3 : j3 + 1;
+                            if (jb3 > p3) continue;
+                            double fb = b == 2 ? chi3[jb3] : dchi3[jb3];
+                            gA[a][b] += fa * fb * C[a][b] * wm;
+                            gAt[a][b] += dchi3[ia3] * dchi3[jb3] * wq;
+                        }
+                    }
+                }
+                for (int j2 = 0; j2 < q2; ++j2)
+                    for (int i2 = 0; i2 < q2; ++i2)
+                        for (int a = 0; a < 3; ++a) {
+                            int ia2 = a == 1 ? i2 : i2 + 1;
+                            if (ia2 > p2) continue;
+                            double fa = a == 1 ? chi2[ia2] : dchi2[ia2];
+                            for (int b = 0; b < 3; ++b) {
+                                int jb2 = b == 1 ? j2 : j2 + 1;
+                                if (jb2 > p2) continue;
+                                double fb = b == 1 ? chi2[jb2] : dchi2[jb2];
+                                GB(gB, a, b, i2, j2) += fa * fb * gA[a][b] * wt[m];
+                                GB(gBt, a, b, i2, j2) += dchi2[ia2] * dchi2[jb2] * gAt[a][b] * wt[m];
+                            }
+                        }
+            }
+            for (int j2 = 0; j2 < q2; ++j2)
+                for (int i2 = 0; i2 < q2; ++i2)
+                    for (int j1 = 0; j1 < q1; ++j1)
+                        for (int i1 = 0; i1 < q1; ++i1)
+                            for (int a = 0; a < 3; ++a) {
+                                if ((a != 0 && i1 >= p1) || (a != 1 && i2 >= p2) || (a != 2 && i3 >= p3)) continue;
+                                int ia1 = a == 0 ? i1 : i1 + 1;
+                                int I = flat_hdiv(a, i1, i2, i3, p1, p2, p3);
+                                for (int b = 0; b < 3; ++b) {
+                                    if ((b != 0 && j1 >= p1) || (b != 1 && j2 >= p2) || (b != 2 && j3 >= p3)) continue;
+                                    int jb1 = b == 0 ? j1 : j1 + 1;
+                                    int Jf = flat_hdiv(b, j1, j2, j3, p1, p2, p3);
+                                    if (I >= Jf) {
+                                        int rs = 2 * (a == 0 ? 0 : 1) + (b == 0 ? 0 : 1);
+                                        G[(size_t)I * N + Jf] += FT(rs, ia1, jb1) * GB(gB, a, b, i2, j2) +
+                                                                 FT(3, ia1, jb1) * GB(gBt, a, b, i2, j2);
+                                        acc += 2;
+                                    }
+                                }
+                            }
+        }
+#undef GB
+    free(gB);
+    free(gBt);
+    mirror_lower(G, N);
+    return acc;
+}
+
+/* _kernels.py:1640-1764 (simp_hcurl_ext) with _rs_hcurl_curl (1313-1324) */
+static long long simp_hcurl_ext(int p1, int p2, int p3, const double *fall, int nF, int L,
+                                const double *nd, const double *wt, int kind, const double *par,
+                                double wmass, double *G)
+{
+    int q1 = p1 + 1, q2 = p2 + 1, q3 = p3 + 1, N = orc_dim(ORC_HCURL, p1, p2, p3);
+    double chi2[64], dchi2[64], chi3[64], dchi3[64], J[3][3], Ji[3][3], D[3][3], C[3][3];
+    double gAc[3][3], gAa[2][2][3][3];
+    double *gBc = malloc(sizeof(double) * 9 * q2 * q2);
+    double *gBa = malloc(sizeof(double) * 36 * q2 * q2);
+#define GBC(a, b, i, j) gBc[(((a) * 3 + (b)) * q2 + (i)) * q2 + (j)]
+#define GBA(al, be, a, b, i, j) gBa[(((((al) * 2 + (be)) * 3 + (a)) * 3 + (b)) * q2 + (i)) * q2 + (j)]
+    long long acc = 0;
+    for (int j3 = 0; j3 < q3; ++j3)
+        for (int i3 = 0; i3 < q3; ++i3) {
+            for (int t = 0; t < 9 * q2 * q2; ++t) gBc[t] = 0.0;
+            for (int t = 0; t < 36 * q2 * q2; ++t) gBa[t] = 0.0;
+            for (int m = 0; m < L; ++m) {
+                orc_shape1_h1(nd[m], p2, chi2, dchi2);
+                memset(gAc, 0, sizeof(gAc));
+                memset(gAa, 0, sizeof(gAa));
+                for (int n = 0; n < L; ++n) {
+                    orc_shape1_h1(nd[n], p3, chi3, dchi3);
+                    double detj = orc_geom_full(kind, par, 0.5, nd[m], nd[n], J, Ji);
+                    metric_d(Ji, D);
+                    metric_c(J, C);
+                    double wqD = wt[n] * detj * wmass;
+                    double wqC = wt[n] / detj;
+                    for (int a = 0; a < 3; ++a) {
+                        int ia3 = a == 2 ? i3 + 1 : i3;
+                        if (ia3 > p3) continue;
+                        double va = a == 2 ? dchi3[ia3] : chi3[ia3];
+                        for (int b = 0; b < 3; ++b) {
+                            int jb3 = b == 2 ? j3 + 1 : j3;
+                            if (jb3 > p3) continue;
+                            double vb = b == 2 ? dchi3[jb3] : chi3[jb3];
+                            gAc[a][b] += va * vb * D[a][b] * wqD;
+                            for (int al = 0; al < 2; ++al) {
+                                int ca = (a + al + 1) % 3;
+                                double fa = ca == 2 ? chi3[ia3] : dchi3[ia3];
+                                for (int be = 0; be < 2; ++be) {
+                                    int cb = (b + be + 1) % 3;
+                                    double fb = cb == 2 ? chi3[jb3] : dchi3[jb3];
+                                    gAa[al][be][a][b] += fa * fb * C[ca][cb] * wqC;
+                                }
+                            }
+                        }
+                    }
+                }
+                for (int j2 = 0; j2 < q2; ++j2)
+                    for (int i2 = 0; i2 < q2; ++i2)
+                        for (int a = 0; a < 3; ++a) {
+                            int ia2 = a == 1 ? i2 + 1 : i2;
+                            if (ia2 > p2) continue;
+                            double va = a == 1 ? dchi2[ia2] : chi2[ia2];
+                            for (int b = 0; b < 3; ++b) {
+                                int jb2 = b == 1 ? j2 + 1 : j2;
+                                if (jb2 > p2) continue;
+                                double vb = b == 1 ? dchi2[jb2] : chi2[jb2];
+                                GBC(a, b, i2, j2) += va * vb * gAc[a][b] * wt[m];
+                                for (int al = 0; al < 2; ++al) {
+                                    int ca = (a + al + 1) % 3;
+                                    double fa = ca == 1 ? chi2[ia2] : dchi2[ia2];
+                                    for (int be = 0; be < 2; ++be) {
+                                        int cb = (b + be + 1) % 3;
+                                        double fb = cb == 1 ? chi2[jb2] : dchi2[jb2];
+                                        GBA(al, be, a, b, i2, j2) += fa * fb * gAa[al][be][a][b] * wt[m];
+                                    }
+                                }
+                            }
+                        }
+            }
+            for (int j2 = 0; j2 < q2; ++j2)
+                for (int i2 = 0; i2 < q2; ++i2)
+                    for (int j1 = 0; j1 < q1; ++j1)
+                        for (int i1 = 0; i1 < q1; ++i1)
+                            for (int a = 0; a < 3; ++a) {
+                                if ((a == 0 && i1 >= p1) || (a == 1 && i2 >= p2) || (a == 2 && i3 >= p3)) continue;
+                                int ia1 = a == 0 ? i1 + 1 : i1;
+                                int I = flat_hcurl(a, i1, i2, i3, p1, p2, p3);
+                                for (int b = 0; b < 3; ++b) {
+                                    if ((b == 0 && j1 >= p1) || (b == 1 && j2 >= p2) || (b == 2 && j3 >= p3)) continue;
+                                    int jb1 = b == 0 ? j1 + 1 : j1;
+                                    int Jf = flat_hcurl(b, j1, j2, j3, p1, p2, p3);
+                                    if (I >= Jf) {
+                                        int rs = 2 * (a == 0 ? 1 : 0) + (b == 0 ? 1 : 0);
+                                        double val = FT(rs, ia1, jb1) * GBC(a, b, i2, j2);
+                                        ++acc;
+                                        for (int al = 0; al < 2; ++al)
+                                            for (int be = 0; be < 2; ++be) {
+                                                double sgn = al == be ? 1.0 : -1.0;
+                                                int ca = (a + al + 1) % 3, cb = (b + be + 1) % 3;
+                                                int rc = 2 * (ca == 0 ? 0 : 1) + (cb == 0 ? 0 : 1);
+                                                val += sgn * FT(rc, ia1, jb1) * GBA(al, be, a, b, i2, j2);
+                                                ++acc;
+                                            }
+                                        G[(size_t)I * N + Jf] += val;
+                                    }
+                                }
+                            }
+        }
+#undef GBC
+#undef GBA
+    free(gBc);
+    free(gBa);
+    mirror_lower(G, N);
+    return acc;
+}
 #undef FT
 
 /* ------------------------------------------------------------------ */
@@ -831,6 +1134,8 @@ static long long simp_hcurl(int p1, int p2, int p3, const double *fall, int nF, 
 /* One element, full N x N matrix (what gram.py:139-158 / 161-205 return).
  * path 0: tensorized (gram_tensorized), wgrid[L^3] may be NULL (-> coef).
  * path 1: simplified constant-Jacobian (gram_simplified), kinds 0..2 only.
+ * path 2: simplified extrusion (gram_simplified, simp_*_ext), kinds 0..3, rule L
+ *         in (xi2, xi3).
  * Returns the accumulation counter, or -1 on a bad argument. */
 long long orc_gram_full(int space, int path, int p1, int p2, int p3, int L,
                         const double *nodes, const double *weights,
@@ -859,7 +1164,7 @@ long long orc_gram_full(int space, int path, int p1, int p2, int p3, int L,
         free(wg);
         return acc;
     }
-    if (kind > 2) return -1; /* gram.py:170-174: only constant-Jacobian kinds here */
+    if (path == ORC_EXTRUSION ? kind > 3 : kind > 2) return -1; /* gram.py:170-174 */
     int pm = p1 > p2 ? p1 : p2;
     pm = pm > p3 ? pm : p3;
     int pF = pm + 1 > 2 ? pm + 1 : 2; /* gram.py:228-231 */
@@ -867,6 +1172,17 @@ long long orc_gram_full(int space, int path, int p1, int p2, int p3, int L,
     double *fall = malloc(sizeof(double) * 4 * nF * nF);
     orc_ftable(pF, fall);
     long long acc = -1;
+    if (path == ORC_EXTRUSION) { /* gram.py:192-203: rule in (xi2, xi3), F tables in xi1 */
+        if (L < 1 || L > 32 || !nodes || !weights) { free(fall); return -1; }
+        switch (space) {
+        case ORC_L2: acc = simp_l2_ext(p1, p2, p3, fall, nF, L, nodes, weights, kind, par, coef, G); break;
+        case ORC_H1: acc = simp_h1_ext(p1, p2, p3, fall, nF, L, nodes, weights, kind, par, coef, G); break;
+        case ORC_HDIV: acc = simp_hdiv_ext(p1, p2, p3, fall, nF, L, nodes, weights, kind, par, coef, G); break;
+        case ORC_HCURL: acc = simp_hcurl_ext(p1, p2, p3, fall, nF, L, nodes, weights, kind, par, coef, G); break;
+        }
+        free(fall);
+        return acc;
+    }
     switch (space) {
     case ORC_L2: acc = simp_l2(p1, p2, p3, fall, nF, kind, par, coef, G); break;
     case ORC_H1: acc = simp_h1(p1, p2, p3, fall, nF, kind, par, coef, G); break;
@@ -926,7 +1242,7 @@ int orc_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E,
     int N = orc_dim(space, p1, p2, p3);
     if (N <= 0 || E < 0) return -1;
     double nodes[32], weights[32];
-    if (path == ORC_GENERAL && orc_gauss_rule(L, nodes, weights) != 0) return -1;
+    if (path != ORC_AFFINE && orc_gauss_rule(L, nodes, weights) != 0) return -1;
     orc_job job = {space, path, p1, p2, p3, L, E, N, kind, params, coef, wgrid, out,
                    nodes, weights, 0, 0};
     if (nthreads <= 0) nthreads = orc_num_cpus();

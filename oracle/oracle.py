@@ -16,7 +16,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 SPACE_CODES = {"H1": 0, "Hcurl": 1, "Hdiv": 2, "L2": 3}
-PATH_CODES = {"general": 0, "affine": 1}
+PATH_CODES = {"general": 0, "affine": 1, "extrusion": 2}
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
@@ -103,7 +103,7 @@ def gram_full(space: str, path: str, orders, L: int, kind: int, params, coef=1.0
               wgrid=None, nodes=None, weights=None):
     """One element, full N x N matrix and the accumulation counter."""
     N = dim(space, orders)
-    if nodes is None and path == "general":
+    if nodes is None and path != "affine":
         nodes, weights = gauss_rule(L)
     nodes = np.ascontiguousarray(nodes if nodes is not None else np.zeros(1), dtype=np.float64)
     weights = np.ascontiguousarray(weights if weights is not None else np.zeros(1),

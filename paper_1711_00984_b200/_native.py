@@ -26,7 +26,7 @@ HXG_MAX_ORDER = 12
 HXG_MAX_RULE = 16
 
 SPACE_CODES = {"H1": 0, "Hcurl": 1, "Hdiv": 2, "L2": 3}
-PATH_CODES = {"general": 0, "affine": 1}
+PATH_CODES = {"general": 0, "affine": 1, "extrusion": 2}
 
 # every symbol the header declares (checked by the CPU test suite)
 EXPORTED = (

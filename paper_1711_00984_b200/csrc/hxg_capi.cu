@@ -9,6 +9,7 @@
 
 #include "../../include/hexgram_b200.h"
 #include "hxg_affine_v2.cuh"
+#include "hxg_extrusion.cuh"
 #include "hxg_general_v2.cuh"
 #include "hxg_kernels.cuh"
 #include "hxg_v2_launch.h"
@@ -264,10 +265,10 @@ int elements_per_chunk(const SpacePlan &P, int L, int E, size_t ws_bytes)
 
 int check_common(int space, int path, int p1, int p2, int p3, int L, int E)
 {
-    if (space < 0 || space > 3 || path < 0 || path > 1) return HXG_ERR_SPACE;
+    if (space < 0 || space > 3 || path < 0 || path > 2) return HXG_ERR_SPACE;
     if (p1 < 1 || p2 < 1 || p3 < 1 || p1 > HXG_MAX_ORDER || p2 > HXG_MAX_ORDER || p3 > HXG_MAX_ORDER)
         return HXG_ERR_ORDER;
-    if (path == GENERAL && (L < 1 || L > HXG_MAX_RULE)) return HXG_ERR_ORDER;
+    if (path != AFFINE && (L < 1 || L > HXG_MAX_RULE)) return HXG_ERR_ORDER;
     if (E < 0) return HXG_ERR_ARG;
     return HXG_OK;
 }
@@ -334,6 +335,9 @@ size_t hxg_workspace_size(int space, int path, int p1, int p2, int p3, int L, in
 {
     if (check_common(space, path, p1, p2, p3, L, E) != HXG_OK) return 0;
     if (path == AFFINE || E == 0) return 0;
+    if (path == EXTRUSION && p1 == p2 && p2 == p3 && p1 <= 10 &&
+        !(getenv("HXG_FORCE_GENERIC") && getenv("HXG_FORCE_GENERIC")[0] == '1'))
+        return 0;  // specialized kernel, no metric workspace
     SpacePlan P;
     build_plan(space, p1, p2, p3, P);
     const size_t per = metric_bytes_per_element(P, L);
@@ -424,6 +428,37 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
             if (rc != HXG_OK) return rc;
         }
         return HXG_OK;
+    }
+
+    if (path == EXTRUSION) {
+        // simplified extrusion path (simp_*_ext): compile-time specialized kernel for
+        // isotropic p <= 10; otherwise the general kernels with the same rule compute
+        // the same integral (the xi1 quadrature with L = p + 1 points is exact for an
+        // xi1-independent Jacobian), after the kind check of gram.py:170-174
+        const char *force = getenv("HXG_FORCE_GENERIC");
+        if (p1 == p2 && p2 == p3 && !(force && force[0] == '1')) {
+            ExtArgs x;
+            x.kind = kind;
+            x.params = params;
+            x.coef = coef;
+            x.tables = tables;
+            x.out = out;
+            x.status = status;
+            x.P = Pk;
+            x.E = E;
+            x.rg = 1;
+            x.L = L;
+            int r = 1;
+            switch (space) {
+            case H1: r = launch_ext_H1(p1, x, st); break;
+            case HCURL: r = launch_ext_hcurl(p1, x, st); break;
+            case HDIV: r = launch_ext_hdiv(p1, x, st); break;
+            default: r = launch_ext_l2(p1, x, st); break;
+            }
+            if (r <= 0) return r == 0 ? HXG_OK : HXG_ERR_CUDA;
+        }
+        ext_kind_kernel<<<(E + 255) / 256, 256, 0, st>>>(E, kind, status);
+        if (cudaGetLastError() != cudaSuccess) return HXG_ERR_CUDA;
     }
 
     // general path, low isotropic orders: one fused kernel (geometry evaluated in
@@ -629,7 +664,7 @@ int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, in
     if (const char *c = getenv("HXG_HOST_CHUNK_MB")) chunk_bytes = std::max(1ll, atoll(c)) << 20;  // tuning
     long long ch = std::max<long long>(1, chunk_bytes / (long long)out_bytes_el);
     ch = std::min<long long>(ch, E);
-    size_t ws = path == GENERAL ? hxg_workspace_size(space, path, p1, p2, p3, L, (int)ch) : 0;
+    size_t ws = hxg_workspace_size(space, path, p1, p2, p3, L, (int)ch);
     int *d_kind = (int *)cx.get(0, sizeof(int) * (size_t)E, ok);
     int *d_status = (int *)cx.get(1, sizeof(int) * (size_t)E, ok);
     double *d_params = (double *)cx.get(2, sizeof(double) * 24 * (size_t)E, ok);
@@ -643,7 +678,7 @@ int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, in
     chk(cudaMemcpyAsync(d_kind, kind, sizeof(int) * (size_t)E, cudaMemcpyHostToDevice, s[0]));
     chk(cudaMemcpyAsync(d_params, params, sizeof(double) * 24 * (size_t)E, cudaMemcpyHostToDevice, s[0]));
     if (coef) chk(cudaMemcpyAsync(d_coef, coef, sizeof(double) * (size_t)E, cudaMemcpyHostToDevice, s[0]));
-    rc = hxg_make_tables(path == GENERAL ? L : 1, nullptr, nullptr, d_tab, s[0]);
+    rc = hxg_make_tables(path == AFFINE ? 1 : L, nullptr, nullptr, d_tab, s[0]);
     chk(cudaEventRecord(cx.inputs_ready, s[0]));
     chk(cudaStreamWaitEvent(s[1], cx.inputs_ready, 0));
     int i = 0;

@@ -5,6 +5,7 @@
 #include "hxg_general_v3.cuh"
 #include "hxg_general_v4.cuh"
 #include "hxg_affine_v2.cuh"
+#include "hxg_extrusion.cuh"
 #include "hxg_v2_launch.h"
 
 namespace hxg {
@@ -115,6 +116,18 @@ int launch_aff_hdiv(int p, const AffV2Args &a, cudaStream_t st)
 {
     switch (p) {
 #define HXG_CASE(PP) case PP: return launch_aff_one<PP>(a, st);
+        HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
+        HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#undef HXG_CASE
+    }
+    return 1;
+}
+
+// specialized extrusion-map kernel (simp_*_ext); returns 1 if none exists for p
+int launch_ext_hdiv(int p, const ExtArgs &a, cudaStream_t st)
+{
+    switch (p) {
+#define HXG_CASE(PP) case PP: return launch_ext_t<HDIV, PP>(a, st);
         HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
         HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
 #undef HXG_CASE

@@ -479,6 +479,14 @@ __global__ void __launch_bounds__(AFF_THREADS) affine_kernel(const __grid_consta
 }
 
 // packed upper triangle -> full symmetric matrix
+// status bit 1 for kinds without an extrusion/constant-Jacobian structure on the
+// simplified extrusion path (gram.py:170-174), when the general kernels serve it
+__global__ void ext_kind_kernel(int E, const int *__restrict__ kind, int *__restrict__ status)
+{
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E && kind[e] > 3) atomicOr(status + e, 2);
+}
+
 __global__ void expand_kernel(int N, long long total, const double *__restrict__ packed,
                               double *__restrict__ full)
 {

@@ -27,7 +27,7 @@
 namespace hxg {
 
 enum Space : int { H1 = 0, HCURL = 1, HDIV = 2, L2 = 3 };
-enum Path : int { GENERAL = 0, AFFINE = 1 };
+enum Path : int { GENERAL = 0, AFFINE = 1, EXTRUSION = 2 };
 
 // 1D table block layout (doubles), built by hxg_make_tables
 constexpr int KT = 16;   // 1D function index capacity (k <= 15, p <= 12 needs k <= 13)

@@ -6,6 +6,7 @@
 namespace hxg {
 struct V2Args;
 struct AffV2Args;
+struct ExtArgs;
 int launch_v2_H1(int p, const V2Args &a, cudaStream_t st);
 int launch_v2_hcurl(int p, const V2Args &a, cudaStream_t st);
 int launch_v2_hdiv(int p, const V2Args &a, cudaStream_t st);
@@ -14,4 +15,8 @@ int launch_aff_H1(int p, const AffV2Args &a, cudaStream_t st);
 int launch_aff_hcurl(int p, const AffV2Args &a, cudaStream_t st);
 int launch_aff_hdiv(int p, const AffV2Args &a, cudaStream_t st);
 int launch_aff_l2(int p, const AffV2Args &a, cudaStream_t st);
+int launch_ext_H1(int p, const ExtArgs &a, cudaStream_t st);
+int launch_ext_hcurl(int p, const ExtArgs &a, cudaStream_t st);
+int launch_ext_hdiv(int p, const ExtArgs &a, cudaStream_t st);
+int launch_ext_l2(int p, const ExtArgs &a, cudaStream_t st);
 }  // namespace hxg

@@ -126,7 +126,7 @@ class GramEngine:
         e = int(bad[0])
         if s[e] & 2:
             raise SimplificationNotApplicableError(
-                f"element {e}: map kind admits no constant-Jacobian simplification")
+                f"element {e}: map kind admits no {path} simplification")
         raise DegenerateMapError(float("nan"), (e,))
 
     def expand(self, packed: torch.Tensor, N: int, stream=None) -> torch.Tensor:

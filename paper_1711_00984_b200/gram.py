@@ -161,10 +161,9 @@ def gram_tensorized(sig: SpaceSignature, emap: ElementMap, rule1d: Rule1D | None
 def gram_simplified(sig: SpaceSignature, emap: ElementMap, ftab: FTable | None = None,
                     rule1d: Rule1D | None = None, *, mass_weight=None) -> GramResult:
     """Simplified Gram matrix (gram.py:161-205): constant-Jacobian maps on the
-    closed-form O(p^6) kernel.  Extrusion maps are integrated by the general
-    device kernel with the same 1D rule (the extrusion-specific kernel is a
-    listed next step); their values agree with the reference's extrusion
-    backend to its own cross-backend tolerance."""
+    closed-form O(p^6) kernel (path 1, simp_*_const), extrusion maps on the
+    O(p^6) extrusion kernel (path 2, simp_*_ext: F tables in xi1, the 1D rule
+    squared in (xi2, xi3) at xi1 = 0.5)."""
     klass = classify(emap)
     if klass == "general":
         raise SimplificationNotApplicableError(
@@ -180,7 +179,7 @@ def gram_simplified(sig: SpaceSignature, emap: ElementMap, ftab: FTable | None =
     if rule1d is None:
         rule1d = gauss_rule(default_rule_order(sig.space, sig.orders))
     L = rule1d.nodes.size
-    G = _device_matrix(sig, emap, "general", L, c, None, rule1d)
+    G = _device_matrix(sig, emap, "extrusion", L, c, None, rule1d)
     return GramResult(G, counters(sig.space, sig.orders, "simplified", L, klass="extrusion"))
 
 
@@ -233,8 +232,11 @@ def gram_batched(space: str, orders, kind, params, coef=None, *, path: str = "ge
 
     kind int32 [E], params float64 [E, 24], coef float64 [E] (mass-term
     weight, default 1), optional wgrid float64 [E, L^3]; torch tensors on the
-    device or host arrays.  Returns (packed [E, N(N+1)/2] float64 CUDA tensor,
-    status [E] int32 CUDA tensor) -- row-major upper triangles."""
+    device or host arrays.  path: "general" (gram_tensorized), "affine"
+    (constant-Jacobian gram_simplified) or "extrusion" (extrusion-map
+    gram_simplified, rule_order points in xi2 and xi3).  Returns (packed
+    [E, N(N+1)/2] float64 CUDA tensor, status [E] int32 CUDA tensor) --
+    row-major upper triangles."""
     from .engine import get_engine
 
     sig = SpaceSignature(space, orders)

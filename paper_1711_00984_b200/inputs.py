@@ -62,16 +62,33 @@ def affine_batch(E: int, seed: int, spread: float = 0.2, variable_coef: bool = F
     return ElementBatch(np.full(E, 2, np.int32), params, np.ascontiguousarray(coef))
 
 
+def extrusion_batch(E: int, seed: int, spread: float = 0.1, variable_coef: bool = False):
+    """Extrusion maps (kind 3, geometry.py:100-111): x1 = lam1 xi1 + shift1 with
+    lam1 = 1 + U(-0.2, 0.2), shift1 = U(0, 1), and the planar quad
+    (v00, v10, v01, v11) = unit-square corners + U(-spread, spread)^(4, 2)."""
+    rng = np.random.default_rng(seed)
+    lam1 = 1.0 + rng.uniform(-0.2, 0.2, E)
+    shift1 = rng.uniform(0.0, 1.0, E)
+    quad = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [1.0, 1.0]])
+    verts = quad[None] + rng.uniform(-spread, spread, (E, 4, 2))
+    params = np.zeros((E, 24))
+    params[:, 0] = lam1
+    params[:, 1] = shift1
+    params[:, 2:10] = verts.reshape(E, 8)
+    coef = rng.uniform(0.5, 2.0, E) if variable_coef else np.ones(E)
+    return ElementBatch(np.full(E, 3, np.int32), params, np.ascontiguousarray(coef))
+
+
 @dataclass(frozen=True)
 class Workload:
     name: str
     space: str
     p: int
     L: int
-    path: str  # "general" (O(p^7)) or "affine" (O(p^6))
+    path: str  # "general" (O(p^7)), "affine" or "extrusion" (O(p^6))
     E: int
     seed: int
-    maps: str  # "trilinear" | "affine"
+    maps: str  # "trilinear" | "affine" | "extrusion"
     variable_coef: bool = False
 
     @property
@@ -82,6 +99,8 @@ class Workload:
         E = self.E if E is None else E
         if self.maps == "trilinear":
             return trilinear_batch(E, self.seed, variable_coef=self.variable_coef)
+        if self.maps == "extrusion":
+            return extrusion_batch(E, self.seed, variable_coef=self.variable_coef)
         return affine_batch(E, self.seed, variable_coef=self.variable_coef)
 
 
@@ -132,4 +151,13 @@ SWEEP_WORKLOADS = {
     for sp in ("H1", "Hcurl", "Hdiv") for p in range(2, 11)
     for path, maps in (("general", "trilinear"), ("affine", "affine"))
 }
-ALL_WORKLOADS = {**WORKLOADS, **SWEEP_WORKLOADS}
+# extrusion-map simplified path (not a BASELINE config):
+# the config-3 shape on extrusion maps, and the order sweep of config 5
+EXTRUSION_WORKLOADS = {
+    "x_hcurl_p6_extrusion": Workload("x_hcurl_p6_extrusion", "Hcurl", 6, 7, "extrusion", 2048, 5,
+                                     "extrusion"),
+    **{f"x5_{sp.lower()}_p{p}_extrusion": Workload(f"x5_{sp.lower()}_p{p}_extrusion", sp, p, p + 1,
+                                                    "extrusion", sweep_elements(sp, p), 4, "extrusion")
+       for sp in ("H1", "Hcurl", "Hdiv") for p in range(2, 11)},
+}
+ALL_WORKLOADS = {**WORKLOADS, **SWEEP_WORKLOADS, **EXTRUSION_WORKLOADS}

@@ -37,7 +37,7 @@ def golden_cases(g):
         pre = f"case{i:03d}"
         meta = g[pre + "_meta"]
         out.append(dict(
-            space=spaces[int(meta[0])], path="affine" if meta[1] else "general",
+            space=spaces[int(meta[0])], path=("general", "affine", "extrusion")[int(meta[1])],
             orders=tuple(int(x) for x in meta[2:5]), L=int(meta[5]), kind=int(meta[6]),
             acc=int(meta[7]), params=g[pre + "_params"], coef=float(g[pre + "_coef"][0]),
             wgrid=g[pre + "_wgrid"] if (pre + "_wgrid") in g.files else None,

@@ -32,6 +32,7 @@ from paper_1711_00984_b200.inputs import WORKLOADS, dim  # noqa: E402
 OUT = os.path.join(HERE, "golden_ref.npz")
 SPACES = ("H1", "Hcurl", "Hdiv", "L2")
 MAPS = ("identity", "diagonal-affine", "general-affine", "trilinear")
+PATHS = ("general", "affine", "extrusion")  # meta[1]
 
 
 def packed(G):
@@ -90,6 +91,21 @@ def main():
                     res = hg.gram_simplified(sig, em, mass_weight=coef)
                     cases.append((space, "affine", orders, L, em.kind_code, em.params, coef,
                                   None, res.matrix, res.counters.accumulations))
+    # simplified extrusion path (gram.py:192-203 -> simp_*_ext, _kernels.py:1405-1764):
+    # the preset map and a seeded random extrusion, default rule (L2: L = max p)
+    rng_x = np.random.default_rng(11)
+    quad = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [1.0, 1.0]])
+    ext_maps = [preset_map("extrusion"),
+                hg.extrusion_map(0.8, 0.3, quad + rng_x.uniform(-0.15, 0.15, (4, 2)))]
+    for space in SPACES:
+        for orders in [(1, 1, 1), (2, 2, 2), (2, 3, 2), (1, 2, 3), (3, 2, 3), (3, 3, 3), (2, 3, 4)]:
+            for k, em in enumerate(ext_maps):
+                sig = hg.SpaceSignature(space, orders)
+                coef = 1.0 if k == 0 else 1.4
+                L = hg.default_rule_order(space, orders)
+                res = hg.gram_simplified(sig, em, mass_weight=coef)
+                cases.append((space, "extrusion", orders, L, em.kind_code, em.params, coef, None,
+                              res.matrix, res.counters.accumulations))
     # reference default rule order for L2 is max(p) (quadrature.py:86-89)
     for orders in [(2, 2, 2), (3, 2, 3)]:
         em = preset_map("trilinear")
@@ -110,7 +126,7 @@ def main():
                       res.matrix, res.counters.accumulations))
     for i, (space, path, orders, L, kind, par, coef, wg, G, acc) in enumerate(cases):
         pre = f"case{i:03d}"
-        d[pre + "_meta"] = np.array([SPACES.index(space), path == "affine", *orders, L, kind, acc],
+        d[pre + "_meta"] = np.array([SPACES.index(space), PATHS.index(path), *orders, L, kind, acc],
                                     np.int64)
         d[pre + "_params"] = par
         d[pre + "_coef"] = np.array([coef])

@@ -64,7 +64,7 @@ def test_accumulation_counters_match_reference(lib, golden):
     (read from the golden cases the reference produced)."""
     codes = {"H1": 0, "Hcurl": 1, "Hdiv": 2, "L2": 3}
     for c in golden_cases(golden):
-        path = 0 if c["path"] == "general" else 1
+        path = {"general": 0, "affine": 1, "extrusion": 2}[c["path"]]
         assert lib.hxg_accumulations(codes[c["space"]], path, *c["orders"], c["L"]) == c["acc"]
 
 

@@ -85,7 +85,7 @@ def test_golden_cases_dropin_api(golden):
         kind_name = {0: "identity", 1: "diagonal-affine", 2: "general-affine", 3: "extrusion",
                      4: "trilinear"}[c["kind"]]
         em = hx.ElementMap(kind_name, c["params"])
-        if c["path"] == "affine":
+        if c["path"] in ("affine", "extrusion"):
             res = hx.gram_simplified(sig, em, mass_weight=c["coef"])
         elif c["wgrid"] is not None:
             w = lambda x: 1.0 + x[0] ** 2 + 0.5 * x[1]  # noqa: E731 (make_golden.py)
@@ -301,3 +301,81 @@ def test_affine_row_group_split_invariant(space, p, monkeypatch, orc):
     ref = orc.gram_batched(space, "affine", (p, p, p), 1, b.kind, b.params, b.coef)
     rel = np.linalg.norm(outs[0] - ref, axis=1) / np.linalg.norm(ref, axis=1)
     assert rel.max() <= TOL
+
+
+# ---------------------------------------------------------------------------
+# simplified extrusion path (path 2, simp_*_ext, _kernels.py:1405-1764)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("space", SPACES)
+@pytest.mark.parametrize("orders", [(1, 1, 1), (2, 2, 2), (3, 3, 3), (2, 3, 2), (1, 2, 3), (4, 4, 4),
+                                    (5, 5, 5), (6, 6, 6), (7, 7, 7), (8, 8, 8), (10, 10, 10)])
+def test_extrusion_vs_oracle(space, orders, orc):
+    """Extrusion maps through the C ABI (specialized kernel for isotropic p <= 10,
+    the general kernels for anisotropic orders) against the C restatement of
+    simp_*_ext, at the reference's default rule (L = p + 1, L2: p)."""
+    from paper_1711_00984_b200.inputs import extrusion_batch
+    from paper_1711_00984_b200.quadrature import default_rule_order
+
+    b = extrusion_batch(4 if max(orders) < 8 else 2, 600 + sum(orders), variable_coef=True)
+    check_batch(space, "extrusion", orders, default_rule_order(space, orders), b, orc)
+
+
+@pytest.mark.parametrize("space", SPACES)
+def test_extrusion_rule_orders(space, orc):
+    """Rules other than the default (gram(..., rule_order=L)) on the extrusion path."""
+    from paper_1711_00984_b200.inputs import extrusion_batch
+
+    b = extrusion_batch(3, 650, variable_coef=True)
+    for L in (2, 5, 9, 16):
+        check_batch(space, "extrusion", (4, 4, 4), L, b, orc)
+
+
+def test_extrusion_equals_general_on_extrusion_maps():
+    """Same integral on two algorithms: the xi1 rule of the general path with
+    L = p + 1 is exact for an xi1-independent Jacobian."""
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import extrusion_batch
+
+    for space in SPACES:
+        for p in (2, 5, 7):
+            b = extrusion_batch(8, 700 + p, variable_coef=True)
+            x, _ = gram_batched(space, (p, p, p), b.kind, b.params, b.coef, path="extrusion",
+                                rule_order=p + 1)
+            g, _ = gram_batched(space, (p, p, p), b.kind, b.params, b.coef, rule_order=p + 1)
+            torch.cuda.synchronize()
+            rel = torch.linalg.norm(x - g, dim=1) / torch.linalg.norm(g, dim=1)
+            assert float(rel.max()) <= TOL, (space, p, float(rel.max()))
+
+
+def test_extrusion_path_rejects_trilinear_maps():
+    import paper_1711_00984_b200 as hx
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.inputs import extrusion_batch, trilinear_batch
+
+    b = trilinear_batch(2, 5)
+    with pytest.raises(hx.SimplificationNotApplicableError):
+        gram_batched("H1", (3, 3, 3), b.kind, b.params, b.coef, path="extrusion")
+    with pytest.raises(hx.SimplificationNotApplicableError):  # anisotropic: general-kernel route
+        gram_batched("H1", (2, 3, 2), b.kind, b.params, b.coef, path="extrusion")
+    x = extrusion_batch(2, 6)
+    x.params[1, 2:10] = x.params[1, [4, 5, 2, 3, 6, 7, 8, 9]]  # swap v00 <-> v10: det < 0
+    with pytest.raises(hx.DegenerateMapError):
+        gram_batched("H1", (3, 3, 3), x.kind, x.params, x.coef, path="extrusion")
+
+
+def test_extrusion_host_entry_matches_device_entry():
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.engine import get_engine
+    from paper_1711_00984_b200.inputs import dim, extrusion_batch
+
+    b = extrusion_batch(37, 710, variable_coef=True)
+    dev, _ = gram_batched("Hcurl", (4, 4, 4), b.kind, b.params, b.coef, path="extrusion")
+    N = dim("Hcurl", (4, 4, 4))
+    out = np.empty((37, N * (N + 1) // 2))
+    get_engine().integrate_host("Hcurl", "extrusion", (4, 4, 4), 5, b.kind, b.params, b.coef, out)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out, dev.cpu().numpy())
