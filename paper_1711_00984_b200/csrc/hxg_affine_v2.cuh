@@ -80,7 +80,8 @@ struct AffCfg {
 // test digit i1 (and hence its F factors) fixed and walks column groups K with stride
 // KW = 32 / n1a, so each warp store covers KW * n1a consecutive doubles of the row.
 template <int S, int P, int A, int B>
-__device__ __forceinline__ void aff_rows(const double *smem, double *__restrict__ outE, int j2, int j3)
+__device__ __forceinline__ void aff_rows(const double *smem, double *__restrict__ outE, int j2, int j3,
+                                         int bs_off = 0)  // bs_off: doubles past OFF_B (extrusion j2 slots)
 {
     using C = AffCfg<S, P>;
     constexpr CPair pp = make_pair_plan(S, A, B);
@@ -91,7 +92,7 @@ __device__ __forceinline__ void aff_rows(const double *smem, double *__restrict_
     constexpr int offA = C::off(A), offB = C::off(B);
     constexpr int KW = n1a <= 32 ? 32 / n1a : 1;
     const double *sF = smem + C::OFF_F;
-    const double *sBs = smem + C::OFF_B + A * C::NK * 4;
+    const double *sBs = smem + C::OFF_B + bs_off + A * C::NK * 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int kq = lane / n1a, i1 = lane - kq * n1a;
     const bool act = kq < KW;

@@ -448,6 +448,7 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
             x.E = E;
             x.rg = 1;
             x.L = L;
+            x.jc = 1;
             int r = 1;
             switch (space) {
             case H1: r = launch_ext_H1(p1, x, st); break;

@@ -11,12 +11,13 @@
 // j2 of the slab; rg slabs per CTA (aff_row_groups at slab granularity):
 //   stage A  Abar_g[a][i3][m] = sum_{t in g} sign_t sum_n M_t[m][n] u(i3,n) u(j3,n)
 //            (once per slab, for every test block a >= b)
-//   per j2:
+//   per pass of jc trial digits j2 (shared-memory budget):
 //   stage B  Bs_h[a][(i2,i3)] = sum_{g in h} sum_m u(i2,m) u(j2,m) Abar_g[a][i3][m]
 //   rows     G[J][I] = sum_h F_h[i1][j1] Bs_h[(i2,i3)]        (aff_rows, shared)
 // with the per-point term fields M_t (w_m w_n folded in, hxg_geom.cuh) evaluated
 // once per CTA in shared memory.  The output stream dominates: HBM-write bound.
 #pragma once
+#include <algorithm>
 #include "hxg_affine_v2.cuh"
 
 namespace hxg {
@@ -30,6 +31,7 @@ struct ExtArgs {
     int E;
     int rg;  // row groups per CTA (aff_row_groups)
     int L;   // rule order in xi2 and xi3 (gram.py:192-195)
+    int jc;  // trial digits j2 whose Bs sums are built per pass (host: smem budget)
 };
 
 template <int S, int P>
@@ -52,7 +54,9 @@ struct ExtCfg {
     static constexpr int OFF_T = A::SMEM_BYTES / 8;
     static constexpr int OFF_M = OFF_T + 2 * KT * LT;
     __host__ __device__ static constexpr int off_abar(int L) { return OFF_M + NF * L * L; }
-    __host__ __device__ static constexpr int smem_bytes(int L) { return (off_abar(L) + NB * N3 * NG * L) * 8; }
+    __host__ __device__ static constexpr int off_bs(int L) { return (off_abar(L) + NB * N3 * NG * L + 1) & ~1; }  // double2
+    static constexpr int BS_SLOT = NB * NK * 4;  // Bs of one j2, every test block
+    __host__ __device__ static constexpr int smem_bytes(int L, int jc) { return (off_bs(L) + jc * BS_SLOT) * 8; }
 };
 
 // stage A for test block A of the (A, B) pair: Abar[A][i3][g][m]
@@ -89,7 +93,7 @@ __device__ __forceinline__ void ext_stage_a(double *smem, int Lr, int j3)
 
 // stage B for test block A of the (A, B) pair: Bs_h[A][k = i2 + n2a i3][h]
 template <int S, int P, int LC, int A, int B>
-__device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2)
+__device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2lo, int jn)
 {
     using C = ExtCfg<S, P>;
     constexpr CPair pp = make_pair_plan(S, A, B);
@@ -98,7 +102,8 @@ __device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2)
     const int L = LC ? LC : Lr;
     const double *sT = smem + C::OFF_T;
     const double *sAb = smem + C::off_abar(L) + (size_t)A * N3 * NG * L;
-    for (int k = threadIdx.x; k < n2a * n3a; k += AFF2_THREADS) {
+    for (int it = threadIdx.x; it < jn * n2a * n3a; it += AFF2_THREADS) {
+        const int jj = it / (n2a * n3a), k = it - jj * (n2a * n3a), j2 = j2lo + jj;
         const int i2 = k % n2a, i3 = k / n2a;
         double acc[MAXH] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -112,7 +117,7 @@ __device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2)
                 if (LC || m < L) s = fma(Ta[m] * Tb[m], Ab[m], s);
             acc[pp.g_h[g]] += s;
         }
-        double2 *dst = reinterpret_cast<double2 *>(smem + C::A::OFF_B + (A * C::NK + k) * 4);
+        double2 *dst = reinterpret_cast<double2 *>(smem + C::off_bs(L) + jj * C::BS_SLOT + (A * C::NK + k) * 4);
         dst[0] = make_double2(acc[0], acc[1]);
         dst[1] = make_double2(acc[2], acc[3]);
     }
@@ -143,36 +148,36 @@ __device__ __forceinline__ void ext_stage_a_all(double *smem, int L, int b, int 
 }
 
 template <int S, int P, int LC>
-__device__ __forceinline__ void ext_stage_b_all(double *smem, int L, int b, int j2)
+__device__ __forceinline__ void ext_stage_b_all(double *smem, int L, int b, int j2lo, int jn)
 {
     if constexpr (ExtCfg<S, P>::NB == 1) {
-        ext_stage_b<S, P, LC, 0, 0>(smem, L, j2);
+        ext_stage_b<S, P, LC, 0, 0>(smem, L, j2lo, jn);
     } else if (b == 0) {
-        ext_stage_b<S, P, LC, 0, 0>(smem, L, j2);
-        ext_stage_b<S, P, LC, 1, 0>(smem, L, j2);
-        ext_stage_b<S, P, LC, 2, 0>(smem, L, j2);
+        ext_stage_b<S, P, LC, 0, 0>(smem, L, j2lo, jn);
+        ext_stage_b<S, P, LC, 1, 0>(smem, L, j2lo, jn);
+        ext_stage_b<S, P, LC, 2, 0>(smem, L, j2lo, jn);
     } else if (b == 1) {
-        ext_stage_b<S, P, LC, 1, 1>(smem, L, j2);
-        ext_stage_b<S, P, LC, 2, 1>(smem, L, j2);
+        ext_stage_b<S, P, LC, 1, 1>(smem, L, j2lo, jn);
+        ext_stage_b<S, P, LC, 2, 1>(smem, L, j2lo, jn);
     } else {
-        ext_stage_b<S, P, LC, 2, 2>(smem, L, j2);
+        ext_stage_b<S, P, LC, 2, 2>(smem, L, j2lo, jn);
     }
 }
 
 template <int S, int P>
-__device__ __forceinline__ void ext_rows_all(const double *smem, double *outE, int b, int j2, int j3)
+__device__ __forceinline__ void ext_rows_all(const double *smem, double *outE, int b, int j2, int j3, int off)
 {
     if constexpr (ExtCfg<S, P>::NB == 1) {
-        aff_rows<S, P, 0, 0>(smem, outE, j2, j3);
+        aff_rows<S, P, 0, 0>(smem, outE, j2, j3, off);
     } else if (b == 0) {
-        aff_rows<S, P, 0, 0>(smem, outE, j2, j3);
-        aff_rows<S, P, 1, 0>(smem, outE, j2, j3);
-        aff_rows<S, P, 2, 0>(smem, outE, j2, j3);
+        aff_rows<S, P, 0, 0>(smem, outE, j2, j3, off);
+        aff_rows<S, P, 1, 0>(smem, outE, j2, j3, off);
+        aff_rows<S, P, 2, 0>(smem, outE, j2, j3, off);
     } else if (b == 1) {
-        aff_rows<S, P, 1, 1>(smem, outE, j2, j3);
-        aff_rows<S, P, 2, 1>(smem, outE, j2, j3);
+        aff_rows<S, P, 1, 1>(smem, outE, j2, j3, off);
+        aff_rows<S, P, 2, 1>(smem, outE, j2, j3, off);
     } else {
-        aff_rows<S, P, 2, 2>(smem, outE, j2, j3);
+        aff_rows<S, P, 2, 2>(smem, outE, j2, j3, off);
     }
 }
 
@@ -228,11 +233,14 @@ __global__ void __launch_bounds__(AFF2_THREADS) ext_v2_kernel(const __grid_const
             if (b == bb) n2b = C::n(bb, 1);
         __syncthreads();  // fields ready; previous slab done with Abar / Bs
         ext_stage_a_all<S, P, LC>(smem, L, b, j3);
-        for (int j2 = 0; j2 < n2b; ++j2) {
-            __syncthreads();  // Abar complete; previous row group's rows done with Bs
-            ext_stage_b_all<S, P, LC>(smem, L, b, j2);
+        for (int j2lo = 0; j2lo < n2b; j2lo += args.jc) {
+            const int jn = cmin(args.jc, n2b - j2lo);
+            __syncthreads();  // Abar complete; previous rows done with the Bs slots
+            ext_stage_b_all<S, P, LC>(smem, L, b, j2lo, jn);
             __syncthreads();
-            ext_rows_all<S, P>(smem, outE, b, j2, j3);
+            const int off = C::off_bs(L) - CA::OFF_B;  // aff_rows reads OFF_B + off + slot
+            for (int jj = 0; jj < jn; ++jj)
+                ext_rows_all<S, P>(smem, outE, b, j2lo + jj, j3, off + jj * C::BS_SLOT);
         }
     }
 }
@@ -243,13 +251,19 @@ inline int launch_ext_t(const ExtArgs &a, cudaStream_t st)
 {
     using C = ExtCfg<S, P>;
     constexpr int NS = ext_slabs<S, P>();
-    const size_t smem = C::smem_bytes(a.L);
+    // Bs of jc trial digits per pass (one barrier pair per pass instead of per j2)
+    const int n2max = C::A::nmax(1);
+    long long budget = 24LL * 1024;
+    if (const char *t = getenv("HXG_EXT_SMEM_KB")) budget = 1024LL * atoll(t);  // tuning
+    int jc = (int)std::min<long long>(n2max, std::max<long long>(1, (budget / 8 - C::off_bs(a.L)) / C::BS_SLOT));
+    const size_t smem = C::smem_bytes(a.L, jc);
     if (smem > 200 * 1024) return 1;
     // the reference's default rule (L = p + 1) unrolls; other rules loop
     auto k = a.L == P + 1 ? ext_v2_kernel<S, P, P + 1> : ext_v2_kernel<S, P, 0>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -5;
     ExtArgs b = a;
+    b.jc = jc;
     // slabs per CTA: ~128 KB of output per CTA, >= 16 CTAs per SM (aff_row_groups
     // on slab granularity)
     b.rg = aff_row_groups(NS, a.P, a.E);
