@@ -130,6 +130,46 @@ int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, in
  * layout, gram.py:53-56, mirrored as _kernels.py:161-174 does). */
 int hxg_expand_full(int N, int E, const double *packed, double *full, void *stream);
 
+
+/* ------------------------------------------------------------------------
+ * Direct consumers of the Gram kernels in the reference's DPG layer
+ * (/root/reference/pkg/src/hexgram/dpg.py).
+ * All pointers are DEVICE pointers; stream-ordered, no host sync.
+ * ------------------------------------------------------------------------ */
+
+/* dpg.py:155-176 _graph_mixed_ftables: the adjoint-graph cross block
+ * S[mw][mv] (row-major), mw = (pr+1)^3 (H1 test space), mv = 3 pr^2 (pr+1)
+ * (H(div) test space), S[ih][iv] = omega ((q_i, div v_j) - (grad q_i, v_j))
+ * on the master element, from the closed-form F tables of `tables`
+ * (hxg_make_tables, any L). */
+int hxg_graph_mixed(int pr, double omega, const double *tables, double *S, void *stream);
+
+/* dpg.py:205-219 adjoint_graph_gram: real block form [[re, -im], [im, re]] of
+ * the adjoint-graph Gram, re = diag(Gq, Gv), im = [[0, S], [-S^T, 0]], for E
+ * elements from the packed H1 Gram g_h1 [E][mw(mw+1)/2] and H(div) Gram
+ * g_hdiv [E][mv(mv+1)/2] (hxg_gram_batched with coef = omega^2 + alpha) and
+ * S (NULL: include_mixed=False).  Writes full [E][2m][2m] (m = mw + mv)
+ * and/or packed [E][2m(2m+1)/2] row-major upper triangles (either may be
+ * NULL, not both). */
+int hxg_graph_assemble(int pr, int E, const double *g_h1, const double *g_hdiv, const double *S,
+                       double *full, double *packed, void *stream);
+
+/* Workspace (bytes) hxg_condense_batched wants for E elements of sizes m, n
+ * (it works in chunks; one element's (m+n+1)^2 doubles is the minimum). */
+size_t hxg_condense_workspace_size(int m, int n, int E);
+
+/* dpg.py:348-357 condense, batched: per element A = B^T G^-1 B [n][n] and
+ * rhs = B^T G^-1 l [n] through a Cholesky factorisation of G (partial
+ * Cholesky elimination of [[G, B, l], [B^T, 0], [l^T, 0]], FP64).
+ *   G   : [E][m(m+1)/2] packed upper triangles (the hxg_gram_batched layout)
+ *   B   : [E][m][n] row-major;  l : [E][m] or NULL (rhs = 0)
+ *   A   : [E][n][n];  rhs : [E][n] or NULL
+ *   status : [E] or NULL; bit 2 (value 4) set when a pivot of G is not
+ *            positive (the reference raises NonSPDError, dpg.py:350-353). */
+int hxg_condense_batched(int m, int n, int E, const double *G, const double *B, const double *l,
+                         double *A, double *rhs, int *status, void *workspace, size_t workspace_bytes,
+                         void *stream);
+
 #ifdef __cplusplus
 }
 #endif

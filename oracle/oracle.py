@@ -144,3 +144,77 @@ def unpack(packed: np.ndarray, N: int) -> np.ndarray:
     G[iu] = packed
     G.T[iu] = packed
     return G
+
+
+# ---------------------------------------------------------------------------
+# DPG-layer consumers of the Gram kernels, numpy
+# restatements of /root/reference/pkg/src/hexgram/dpg.py
+# ---------------------------------------------------------------------------
+def _sep3(A1, A2, A3):
+    """dpg.py:146-152: separable triple product, digit-lexicographic (fastest
+    digit first) on both axes; products in einsum operand order."""
+    T = (A1[:, None, None, :, None, None] * A2[None, :, None, None, :, None]) \
+        * A3[None, None, :, None, None, :]
+    # T[i, j, k, x, y, z] -> rows (k, j, i), columns (z, y, x)
+    T = T.transpose(2, 1, 0, 5, 4, 3)
+    r = A1.shape[0] * A2.shape[0] * A3.shape[0]
+    c = A1.shape[1] * A2.shape[1] * A3.shape[1]
+    return T.reshape(r, c)
+
+
+def graph_mixed(pr: int, omega: float) -> np.ndarray:
+    """dpg.py:155-176 _graph_mixed_ftables: S[ih, iv] = omega (q, div v) -
+    omega (grad q, v) on the master element from the closed-form F01 table."""
+    f01 = ftable(pr + 1)[1]
+    q = pr + 1
+    blocks = []
+    for a in range(3):
+        K1, K2 = [], []
+        for d in range(3):
+            n_d = q if d == a else pr
+            sh = 0 if d == a else 1
+            M1 = np.empty((q, n_d))
+            M2 = np.empty((q, n_d))
+            for i in range(q):
+                for j in range(n_d):
+                    M1[i, j] = f01[i, j + sh]
+                    M2[i, j] = f01[j, i] if d == a else f01[i, j + sh]
+            K1.append(M1)
+            K2.append(M2)
+        blocks.append(omega * (_sep3(*K1) - _sep3(*K2)))
+    return np.hstack(blocks)
+
+
+def adjoint_graph_gram(pr: int, omega: float, alpha: float, path: str, kind: int, params,
+                       include_mixed: bool = True) -> np.ndarray:
+    """dpg.py:179-231: real block form [[re, -im], [im, re]] with
+    re = diag(G_H1, G_Hdiv) (mass weight omega^2 + alpha) and
+    im = [[0, S], [-S^T, 0]]."""
+    w = omega * omega + alpha
+    L = pr + 1 if path != "affine" else 1
+    o = (pr, pr, pr)
+    Gq, _ = gram_full("H1", path, o, L, kind, params, coef=w)
+    Gv, _ = gram_full("Hdiv", path, o, L, kind, params, coef=w)
+    mw, mv = Gq.shape[0], Gv.shape[0]
+    m = mw + mv
+    re = np.zeros((m, m))
+    re[:mw, :mw] = Gq
+    re[mw:, mw:] = Gv
+    im = np.zeros((m, m))
+    if include_mixed:
+        S = graph_mixed(pr, omega)
+        im[:mw, mw:] = S
+        im[mw:, :mw] = -S.T
+    return np.block([[re, -im], [im, re]])
+
+
+def condense(G: np.ndarray, B: np.ndarray, l: np.ndarray):
+    """dpg.py:348-357: (B^T G^-1 B, B^T G^-1 l) through the lower Cholesky
+    factor of G (cho_factor / cho_solve restated with numpy); raises
+    numpy.linalg.LinAlgError when G is not positive definite."""
+    from scipy.linalg import solve_triangular
+
+    Lc = np.linalg.cholesky(G)
+    X = solve_triangular(Lc.T, solve_triangular(Lc, B, lower=True), lower=False)
+    y = solve_triangular(Lc.T, solve_triangular(Lc, l, lower=True), lower=False)
+    return B.T @ X, B.T @ y

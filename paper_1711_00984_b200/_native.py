@@ -42,6 +42,10 @@ EXPORTED = (
     "hxg_contract_batched",
     "hxg_gram_batched_host",
     "hxg_expand_full",
+    "hxg_graph_mixed",
+    "hxg_graph_assemble",
+    "hxg_condense_workspace_size",
+    "hxg_condense_batched",
 )
 
 _lib = None
@@ -93,6 +97,14 @@ def lib():
     L.hxg_gram_batched_host.restype = _i
     L.hxg_expand_full.argtypes = [_i, _i, _vp, _vp, _vp]
     L.hxg_expand_full.restype = _i
+    L.hxg_graph_mixed.argtypes = [_i, ctypes.c_double, _vp, _vp, _vp]
+    L.hxg_graph_mixed.restype = _i
+    L.hxg_graph_assemble.argtypes = [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.hxg_graph_assemble.restype = _i
+    L.hxg_condense_workspace_size.argtypes = [_i, _i, _i]
+    L.hxg_condense_workspace_size.restype = _sz
+    L.hxg_condense_batched.argtypes = [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    L.hxg_condense_batched.restype = _i
     _lib = L
     return L
 

@@ -1,0 +1,364 @@
+// hxg_dpg.cu -- the two direct consumers of the Gram kernels in the
+// reference's DPG layer, batched on the device:
+//
+//   * the adjoint-graph Gram of the ultraweak acoustics problem
+//     (/root/reference/pkg/src/hexgram/dpg.py:179-231): diagonal blocks are
+//     the H1 and H(div) Grams with mass weight omega^2 + alpha (produced by
+//     hxg_gram_batched), the off-diagonal block is the closed-form frequency
+//     coupling S (dpg.py:155-176, graph_mixed_kernel below); the element
+//     matrix is stored in real block form [[re, -im], [im, re]]
+//     (dpg.py:211-219, graph_assemble_kernel);
+//   * static condensation (dpg.py:348-357): A = B^T G^-1 B, rhs = B^T G^-1 l
+//     through a Cholesky factor of G.  Here it is one partial Cholesky
+//     elimination of the bordered matrix
+//         M = [[G, B~], [B~^T, 0]],   B~ = [B | l]
+//     over its first m columns: the Schur complement left in the trailing
+//     (n+1) x (n+1) block is -B~^T G^-1 B~ = -[[A, rhs], [rhs^T, .]], so the
+//     Cholesky factor, both triangular solves of cho_solve and the two
+//     products B^T(.) are one right-looking blocked elimination
+//     (condense_kernel), FP64 throughout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "../../include/hexgram_b200.h"
+#include "hxg_plan.h"
+
+using namespace hxg;
+
+namespace {
+
+__device__ __forceinline__ long long packed_index(long long r, long long c, long long N)
+{
+    if (r > c) { const long long t = r; r = c; c = t; }
+    return r * N - r * (r - 1) / 2 + (c - r);
+}
+
+// ---------------------------------------------------------------------------
+// adjoint-graph cross block (dpg.py:155-176):
+//   S_a[(i1,i2,i3), (x1,x2,x3)] = omega (prod_d K1_d - prod_d K2_d)
+//   K1_d = F01[i_d][x_d + sh_d], K2_a = F01[x_a][i_a], K2_d = K1_d (d != a),
+//   sh_d = 0 on the block's own direction a, 1 elsewhere (nu_j = chi'_{j+1})
+// rows: H1 flat index (i1 fastest), columns: H(div) blocks a = 0,1,2 stacked
+// (dpg.py:176 np.hstack), each digit-lexicographic with x1 fastest
+// (_sep3, dpg.py:146-152).  Products in the einsum's operand order.
+// ---------------------------------------------------------------------------
+__global__ void graph_mixed_kernel(int pr, double omega, const double *__restrict__ tab,
+                                   double *__restrict__ S)
+{
+    const int q = pr + 1;
+    const int mw = q * q * q, nb = q * pr * pr, mv = 3 * nb;
+    const double *F01 = tab + TAB_F + KT * KT;
+    const long long total = (long long)mw * mv;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int ih = (int)(idx / mv), iv = (int)(idx - (long long)ih * mv);
+        const int a = iv / nb, x = iv - a * nb;
+        const int i[3] = {ih % q, (ih / q) % q, ih / (q * q)};
+        const int n0 = a == 0 ? q : pr, n1 = a == 1 ? q : pr;
+        const int xd[3] = {x % n0, (x / n0) % n1, x / (n0 * n1)};
+        double k1[3], k2[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            if (d == a) {
+                k1[d] = F01[i[d] * KT + xd[d]];
+                k2[d] = F01[xd[d] * KT + i[d]];
+            } else {
+                k1[d] = k2[d] = F01[i[d] * KT + xd[d] + 1];
+            }
+        }
+        S[idx] = omega * (k1[0] * k1[1] * k1[2] - k2[0] * k2[1] * k2[2]);
+    }
+}
+
+// real block form of the adjoint-graph Gram (dpg.py:205-219):
+//   G = [[re, -im], [im, re]],  re = diag(Gq, Gv),  im = [[0, S], [-S^T, 0]]
+// from the packed H1 Gram gq [E][mw(mw+1)/2], the packed H(div) Gram
+// gv [E][mv(mv+1)/2] and S [mw][mv] (NULL: include_mixed=False).  Writes the
+// full matrices [E][2m][2m] and/or their packed upper triangles.
+__device__ __forceinline__ double graph_entry(long long e, int r, int c, int mw, int mv,
+                                              const double *__restrict__ gq,
+                                              const double *__restrict__ gv,
+                                              const double *__restrict__ S)
+{
+    const int m = mw + mv;
+    const bool br = r >= m, bc = c >= m;
+    const int R = br ? r - m : r, C = bc ? c - m : c;
+    if (br == bc) {
+        if (R < mw && C < mw) return gq[e * ((long long)mw * (mw + 1) / 2) + packed_index(R, C, mw)];
+        if (R >= mw && C >= mw)
+            return gv[e * ((long long)mv * (mv + 1) / 2) + packed_index(R - mw, C - mw, mv)];
+        return 0.0;
+    }
+    if (!S) return 0.0;
+    double im = 0.0;
+    if (R < mw && C >= mw) im = S[(long long)R * mv + (C - mw)];
+    else if (R >= mw && C < mw) im = -S[(long long)C * mv + (R - mw)];
+    return br ? im : -im;
+}
+
+__global__ void graph_assemble_kernel(int mw, int mv, int E, const double *__restrict__ gq,
+                                      const double *__restrict__ gv, const double *__restrict__ S,
+                                      double *__restrict__ full, double *__restrict__ packed)
+{
+    const int M2 = 2 * (mw + mv);
+    const long long NN = (long long)M2 * M2, P = (long long)M2 * (M2 + 1) / 2;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (full) {
+        for (long long idx = t0; idx < (long long)E * NN; idx += stride) {
+            const long long e = idx / NN, rc = idx - e * NN;
+            const int r = (int)(rc / M2), c = (int)(rc - (long long)r * M2);
+            full[idx] = graph_entry(e, r, c, mw, mv, gq, gv, S);
+        }
+    }
+    if (packed) {
+        for (long long idx = t0; idx < (long long)E * P; idx += stride) {
+            const long long e = idx / P;
+            long long k = idx - e * P;
+            // row r of the packed upper triangle holds M2 - r entries
+            int r = (int)((2.0 * M2 + 1 - sqrt((2.0 * M2 + 1) * (2.0 * M2 + 1) - 8.0 * k)) / 2);
+            while (r > 0 && (long long)r * M2 - (long long)r * (r - 1) / 2 > k) --r;
+            while ((long long)(r + 1) * M2 - (long long)(r + 1) * r / 2 <= k) ++r;
+            const int c = r + (int)(k - ((long long)r * M2 - (long long)r * (r - 1) / 2));
+            packed[idx] = graph_entry(e, r, c, mw, mv, gq, gv, S);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// static condensation (dpg.py:348-357) as a partial Cholesky elimination of
+// the bordered matrix M = [[G, B~], [B~^T, 0]], B~ = [B | l], size
+// Mt = m + n + 1.  Working copy: dense row-major lower triangle per element
+// in the workspace (rows i >= j only).
+// ---------------------------------------------------------------------------
+constexpr int CD_THREADS = 256;
+constexpr int CD_NB = 32;  // panel width
+constexpr int CD_TT = 64;  // trailing-update tile (CD_THREADS threads x 4 x 4)
+
+__global__ void condense_init_kernel(int m, int n, int Ec, const double *__restrict__ G,
+                                     const double *__restrict__ B, const double *__restrict__ l,
+                                     double *__restrict__ W)
+{
+    const int Mt = m + n + 1;
+    const long long MM = (long long)Mt * Mt, Pg = (long long)m * (m + 1) / 2;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)Ec * MM;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long e = idx / MM, rc = idx - e * MM;
+        const int i = (int)(rc / Mt), j = (int)(rc - (long long)i * Mt);
+        if (j > i) continue;
+        double v = 0.0;
+        if (i < m) {
+            v = G[e * Pg + packed_index(j, i, m)];
+        } else if (j < m) {
+            const int r = i - m;  // border row: column r of B~
+            v = r < n ? B[(e * m + j) * n + r] : (l ? l[e * m + j] : 0.0);
+        }
+        W[idx] = v;
+    }
+}
+
+__global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, double *__restrict__ Wall,
+                                                              int *__restrict__ status, int e0)
+{
+    const int Mt = m + n + 1;
+    double *__restrict__ W = Wall + (long long)blockIdx.x * Mt * Mt;
+    __shared__ double sD[CD_NB][CD_NB + 1];
+    __shared__ double sPi[CD_NB][CD_TT + 1];  // panel rows of tile ti, transposed [t][row]
+    __shared__ double sPj[CD_NB][CD_TT + 1];  // panel rows of tile tj
+    __shared__ int s_bad;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_bad = 0;
+    for (int k0 = 0; k0 < m; k0 += CD_NB) {
+        const int kb = min(CD_NB, m - k0);
+        // (a) factor the diagonal block (one warp, unblocked, in shared memory)
+        for (int idx = tid; idx < kb * kb; idx += CD_THREADS) {
+            const int i = idx / kb, j = idx - i * kb;
+            sD[i][j] = j <= i ? W[(long long)(k0 + i) * Mt + k0 + j] : 0.0;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            for (int j = 0; j < kb; ++j) {
+                const double d = sD[j][j];
+                if (!(d > 0.0)) {
+                    if (lane == 0) s_bad = 1;
+                }
+                const double ljj = sqrt(fmax(d, 1e-300));
+                __syncwarp();
+                if (lane == 0) sD[j][j] = ljj;
+                for (int i = j + 1 + lane; i < kb; i += 32) sD[i][j] /= ljj;
+                __syncwarp();
+                for (int i = j + 1 + lane; i < kb; i += 32) {
+                    const double lij = sD[i][j];
+                    for (int k = j + 1; k <= i; ++k) sD[i][k] = fma(-lij, sD[k][j], sD[i][k]);
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < kb * kb; idx += CD_THREADS) {
+            const int i = idx / kb, j = idx - i * kb;
+            if (j <= i) W[(long long)(k0 + i) * Mt + k0 + j] = sD[i][j];
+        }
+        // (b) + (c), one 64-row tile ti of the panel at a time: solve the tile's panel
+        // rows x <- x L_D^-T in shared memory (forward substitution, one thread per row),
+        // write them back, then apply the trailing update of the lower triangle
+        //   W[i][j] -= sum_t P[i][t] P[j][t],  i in tile ti, j in tiles tj <= ti
+        // (tiles tj < ti were solved by earlier passes).
+        const int r0 = k0 + kb;
+        const int R = Mt - r0;
+        const int nt = (R + CD_TT - 1) / CD_TT;
+        const int ty = tid / 16, tx = tid % 16;  // 4x4 micro-tile at rows 4 ty, cols 4 tx
+        for (int ti = 0; ti < nt; ++ti) {
+            const int ib = r0 + ti * CD_TT;
+            for (int idx = tid; idx < CD_TT * CD_NB; idx += CD_THREADS) {
+                const int rr = idx / CD_NB, t = idx - rr * CD_NB;
+                sPi[t][rr] = (t < kb && ib + rr < Mt) ? W[(long long)(ib + rr) * Mt + k0 + t] : 0.0;
+            }
+            __syncthreads();
+            if (tid < CD_TT && ib + tid < Mt) {
+                for (int j = 0; j < kb; ++j) {
+                    double x = sPi[j][tid];
+                    for (int t = 0; t < j; ++t) x = fma(-sPi[t][tid], sD[j][t], x);
+                    sPi[j][tid] = x / sD[j][j];
+                }
+            }
+            __syncthreads();
+            for (int idx = tid; idx < CD_TT * CD_NB; idx += CD_THREADS) {
+                const int rr = idx / CD_NB, t = idx - rr * CD_NB;
+                if (t < kb && ib + rr < Mt) W[(long long)(ib + rr) * Mt + k0 + t] = sPi[t][rr];
+            }
+            for (int tj = 0; tj <= ti; ++tj) {
+                const int jb = r0 + tj * CD_TT;
+                if (tj < ti) {
+                    for (int idx = tid; idx < CD_TT * CD_NB; idx += CD_THREADS) {
+                        const int rr = idx / CD_NB, t = idx - rr * CD_NB;
+                        sPj[t][rr] = (t < kb && jb + rr < Mt) ? W[(long long)(jb + rr) * Mt + k0 + t] : 0.0;
+                    }
+                }
+                __syncthreads();
+                const double(*Pj)[CD_TT + 1] = tj < ti ? sPj : sPi;
+                double acc[4][4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+                for (int t = 0; t < kb; ++t) {
+                    double pi[4], pj[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) pi[a] = sPi[t][4 * ty + a];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) pj[b] = Pj[t][4 * tx + b];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc[a][b] = fma(pi[a], pj[b], acc[a][b]);
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const int i = ib + 4 * ty + a;
+                    if (i >= Mt) continue;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int j = jb + 4 * tx + b;
+                        if (j <= i) W[(long long)i * Mt + j] -= acc[a][b];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && s_bad && status) atomicOr(status + e0 + blockIdx.x, 4);
+}
+
+// A = -(Schur block)[0:n, 0:n] (mirrored), rhs = -(Schur block)[n, 0:n]
+__global__ void condense_final_kernel(int m, int n, int Ec, const double *__restrict__ W,
+                                      double *__restrict__ A, double *__restrict__ rhs)
+{
+    const int Mt = m + n + 1;
+    const long long MM = (long long)Mt * Mt, NN = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)Ec * NN;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long e = idx / NN, rc = idx - e * NN;
+        int r = (int)(rc / n), c = (int)(rc - (long long)r * n);
+        if (c > r) { const int t = r; r = c; c = t; }
+        A[idx] = -W[e * MM + (long long)(m + r) * Mt + (m + c)];
+    }
+    if (rhs) {
+        for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)Ec * n;
+             idx += (long long)gridDim.x * blockDim.x) {
+            const long long e = idx / n;
+            const int r = (int)(idx - e * n);
+            rhs[idx] = -W[e * MM + (long long)(m + n) * Mt + (m + r)];
+        }
+    }
+}
+
+int grid_for(long long work, int threads)
+{
+    return (int)std::max<long long>(1, std::min<long long>((work + threads - 1) / threads, 148LL * 16));
+}
+
+}  // namespace
+
+extern "C" {
+
+int hxg_graph_mixed(int pr, double omega, const double *tables, double *S, void *stream)
+{
+    if (pr < 1 || pr + 1 >= KT) return HXG_ERR_ORDER;
+    if (!tables || !S) return HXG_ERR_ARG;
+    const long long q = pr + 1, total = q * q * q * 3 * q * pr * pr;
+    graph_mixed_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(pr, omega, tables, S);
+    return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
+}
+
+int hxg_graph_assemble(int pr, int E, const double *g_h1, const double *g_hdiv, const double *S,
+                       double *full, double *packed, void *stream)
+{
+    if (pr < 1 || pr > HXG_MAX_ORDER) return HXG_ERR_ORDER;
+    if (E < 0 || !g_h1 || !g_hdiv || (!full && !packed)) return HXG_ERR_ARG;
+    if (E == 0) return HXG_OK;
+    const int q = pr + 1, mw = q * q * q, mv = 3 * q * pr * pr;
+    const long long M2 = 2LL * (mw + mv);
+    graph_assemble_kernel<<<grid_for((long long)E * M2 * M2, 256), 256, 0, (cudaStream_t)stream>>>(
+        mw, mv, E, g_h1, g_hdiv, S, full, packed);
+    return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
+}
+
+size_t hxg_condense_workspace_size(int m, int n, int E)
+{
+    if (m < 1 || n < 1 || E < 1) return 0;
+    const size_t per = (size_t)(m + n + 1) * (m + n + 1) * sizeof(double);
+    const size_t target = (size_t)512 << 20;  // chunk the batch to <= 512 MB of working copies
+    const size_t cap = std::max<size_t>(1, target / per);
+    return std::min<size_t>((size_t)E, cap) * per;
+}
+
+int hxg_condense_batched(int m, int n, int E, const double *G, const double *B, const double *l,
+                         double *A, double *rhs, int *status, void *workspace, size_t ws_bytes,
+                         void *stream)
+{
+    if (m < 1 || n < 1 || E < 0) return HXG_ERR_ARG;
+    if (E == 0) return HXG_OK;
+    if (!G || !B || !A) return HXG_ERR_ARG;
+    const size_t per = (size_t)(m + n + 1) * (m + n + 1) * sizeof(double);
+    if (!workspace || ws_bytes < per) return HXG_ERR_WORKSPACE;
+    const int chunk = (int)std::min<size_t>((size_t)E, ws_bytes / per);
+    cudaStream_t st = (cudaStream_t)stream;
+    double *W = (double *)workspace;
+    if (status && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
+    const long long Pg = (long long)m * (m + 1) / 2;
+    for (int e0 = 0; e0 < E; e0 += chunk) {
+        const int Ec = std::min(chunk, E - e0);
+        const long long Mt = m + n + 1;
+        condense_init_kernel<<<grid_for((long long)Ec * Mt * Mt, 256), 256, 0, st>>>(
+            m, n, Ec, G + e0 * Pg, B + (long long)e0 * m * n, l ? l + (long long)e0 * m : nullptr, W);
+        condense_kernel<<<Ec, CD_THREADS, 0, st>>>(m, n, W, status, e0);
+        condense_final_kernel<<<grid_for((long long)Ec * n * n, 256), 256, 0, st>>>(
+            m, n, Ec, W, A + (long long)e0 * n * n, rhs ? rhs + (long long)e0 * n : nullptr);
+    }
+    return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
+}
+
+}  // extern "C"
