@@ -377,6 +377,65 @@ def measure_e2e(ds, steps, world, device):
     return dt, h2d, d2h
 
 
+def dpg_suite(device, fp64, hbm, reps=3):
+    """SURVEY 8(f) rows 2-3 on seeded batches: the adjoint-graph Gram of the
+    ultraweak acoustics problem (dpg.py:179-231, packed real block form) and
+    batched static condensation (dpg.py:348-357).  Condensation FLOPs are the
+    reference algorithm's (cho_factor m^3/3, cho_solve 2 m^2 (n+1), B^T X
+    2 m n (n+1)); the graph Gram is reported against the HBM bytes of its
+    outputs (two packed Grams + the packed 2m x 2m block matrix)."""
+    import torch
+
+    from paper_1711_00984_b200 import gram_batched
+    from paper_1711_00984_b200.dpg import adjoint_graph_gram_batched, condense_batched
+    from paper_1711_00984_b200.inputs import trilinear_batch
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(device)
+        return e0.elapsed_time(e1) / 1e3 / reps
+
+    out = []
+    # adjoint-graph Gram, p_r = 4, trilinear maps
+    pr, E = 4, 512
+    b = trilinear_batch(E, 21)
+    kind = torch.as_tensor(b.kind).to(device)
+    params = torch.as_tensor(b.params).to(device)
+    t = timed(lambda: adjoint_graph_gram_batched(pr, 2.0, 0.5, kind, params))
+    mw, mv = (pr + 1) ** 3, 3 * pr * pr * (pr + 1)
+    m2 = 2 * (mw + mv)
+    byt = 8.0 * (mw * (mw + 1) // 2 + mv * (mv + 1) // 2 + m2 * (m2 + 1) // 2)
+    out.append({"workload": f"dpg_graph_acoustics_p{pr}_general", "elements_per_s": E / t,
+                "ms_per_step": t * 1e3, "bound": "hbm", "hbm_write_gbs": E * byt / t / 1e9,
+                "roofline_frac": E * byt / t / 1e9 / hbm, "N": m2})
+    # condensation: Poisson primal (H1 Gram p_r = 5 from the Gram kernel, trial p0 = 4) and
+    # acoustics real block form (p_r = 4, 2m = 850, trial 2 x 4 x 27)
+    rng = np.random.default_rng(8)
+    for name, m, n, E in (("dpg_condense_poisson_p5", 216, 125, 1024),
+                          ("dpg_condense_acoustics_p4", m2, 2 * 4 * 27, 96)):
+        if name.startswith("dpg_condense_poisson"):
+            bb = trilinear_batch(E, 22, variable_coef=True)
+            G, _ = gram_batched("H1", (5, 5, 5), bb.kind, bb.params, bb.coef)
+        else:
+            G = adjoint_graph_gram_batched(pr, 2.0, 0.5, kind[:E], params[:E])
+        B = torch.as_tensor(rng.standard_normal((E, m, n))).to(device)
+        l = torch.as_tensor(rng.standard_normal((E, m))).to(device)
+        t = timed(lambda: condense_batched(G, B, l, check=False))
+        F = m ** 3 / 3 + 2.0 * m * m * (n + 1) + 2.0 * m * n * (n + 1)
+        out.append({"workload": name, "elements_per_s": E / t, "ms_per_step": t * 1e3,
+                    "bound": "fp64", "fp64_tflops_alg": E * F / t / 1e12,
+                    "roofline_frac": E * F / t / 1e12 / fp64, "m": m, "n": n})
+        del G, B, l
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, wl, world, rank, local):
     import torch
 
@@ -463,6 +522,7 @@ def run_ours(args, wl, world, rank, local):
             del d2
             torch.cuda.empty_cache()
         line["suite"] = suite
+        line["dpg_suite"] = dpg_suite(device, fp64, hbm)
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, n, dt, threads = cpu_rate(wl, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
