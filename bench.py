@@ -417,13 +417,15 @@ def dpg_suite(device, fp64, hbm, reps=3):
     # condensation: Poisson primal (H1 Gram p_r = 5 from the Gram kernel, trial p0 = 4) and
     # acoustics real block form (p_r = 4, 2m = 850, trial 2 x 4 x 27)
     rng = np.random.default_rng(8)
+    pa = 3  # acoustics: test order p_r = 3, trial p0 = 2 (real block form 2m = 416, 2 x 4 x 8)
+    m2a = 2 * ((pa + 1) ** 3 + 3 * pa * pa * (pa + 1))
     for name, m, n, E in (("dpg_condense_poisson_p5", 216, 125, 1024),
-                          ("dpg_condense_acoustics_p4", m2, 2 * 4 * 27, 96)):
+                          (f"dpg_condense_acoustics_p{pa}", m2a, 2 * 4 * 8, 1024)):
         if name.startswith("dpg_condense_poisson"):
             bb = trilinear_batch(E, 22, variable_coef=True)
             G, _ = gram_batched("H1", (5, 5, 5), bb.kind, bb.params, bb.coef)
         else:
-            G = adjoint_graph_gram_batched(pr, 2.0, 0.5, kind[:E], params[:E])
+            G = adjoint_graph_gram_batched(pa, 2.0, 0.5, kind[:E], params[:E])
         B = torch.as_tensor(rng.standard_normal((E, m, n))).to(device)
         l = torch.as_tensor(rng.standard_normal((E, m))).to(device)
         t = timed(lambda: condense_batched(G, B, l, check=False))

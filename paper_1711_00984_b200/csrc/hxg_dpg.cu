@@ -97,31 +97,26 @@ __device__ __forceinline__ double graph_entry(long long e, int r, int c, int mw,
     return br ? im : -im;
 }
 
+// one warp per output row (e, r): coalesced stores, contiguous packed-row reads
 __global__ void graph_assemble_kernel(int mw, int mv, int E, const double *__restrict__ gq,
                                       const double *__restrict__ gv, const double *__restrict__ S,
                                       double *__restrict__ full, double *__restrict__ packed)
 {
     const int M2 = 2 * (mw + mv);
     const long long NN = (long long)M2 * M2, P = (long long)M2 * (M2 + 1) / 2;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (full) {
-        for (long long idx = t0; idx < (long long)E * NN; idx += stride) {
-            const long long e = idx / NN, rc = idx - e * NN;
-            const int r = (int)(rc / M2), c = (int)(rc - (long long)r * M2);
-            full[idx] = graph_entry(e, r, c, mw, mv, gq, gv, S);
+    const int lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+         row < (long long)E * M2; row += nw) {
+        const long long e = row / M2;
+        const int r = (int)(row - e * M2);
+        if (full) {
+            double *dst = full + e * NN + (long long)r * M2;
+            for (int c = lane; c < M2; c += 32) dst[c] = graph_entry(e, r, c, mw, mv, gq, gv, S);
         }
-    }
-    if (packed) {
-        for (long long idx = t0; idx < (long long)E * P; idx += stride) {
-            const long long e = idx / P;
-            long long k = idx - e * P;
-            // row r of the packed upper triangle holds M2 - r entries
-            int r = (int)((2.0 * M2 + 1 - sqrt((2.0 * M2 + 1) * (2.0 * M2 + 1) - 8.0 * k)) / 2);
-            while (r > 0 && (long long)r * M2 - (long long)r * (r - 1) / 2 > k) --r;
-            while ((long long)(r + 1) * M2 - (long long)(r + 1) * r / 2 <= k) ++r;
-            const int c = r + (int)(k - ((long long)r * M2 - (long long)r * (r - 1) / 2));
-            packed[idx] = graph_entry(e, r, c, mw, mv, gq, gv, S);
+        if (packed) {
+            double *dst = packed + e * P + (long long)r * M2 - (long long)r * (r - 1) / 2 - r;
+            for (int c = r + lane; c < M2; c += 32) dst[c] = graph_entry(e, r, c, mw, mv, gq, gv, S);
         }
     }
 }
@@ -158,31 +153,50 @@ __global__ void condense_init_kernel(int m, int n, int Ec, const double *__restr
     }
 }
 
+__device__ __forceinline__ void cd_dmma(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+constexpr int CD_PS = CD_TT + 8;  // panel row stride (doubles): k rows t, t+1 fall in opposite bank halves
+
+// One CTA (8 warps) per element.  Per panel of CD_NB columns:
+//   (a) warp 0 factors the diagonal block L_D (unblocked, shared memory) and forms
+//       L_D^-1 (one column per lane);
+//   (b) per 64-row tile ti of the rows below: X = P L_D^-T as a DMMA product with the
+//       explicit inverse (8 warps, in place in shared memory), written back;
+//   (c) trailing update of the lower triangle W[i][j] -= sum_t X[i][t] X[j][t] for the
+//       64 x 64 tiles (ti, tj <= ti), DMMA 8x8x4 with 2 x 4 accumulator tiles per warp.
 __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, double *__restrict__ Wall,
                                                               int *__restrict__ status, int e0)
 {
     const int Mt = m + n + 1;
     double *__restrict__ W = Wall + (long long)blockIdx.x * Mt * Mt;
-    __shared__ double sD[CD_NB][CD_NB + 1];
-    __shared__ double sPi[CD_NB][CD_TT + 1];  // panel rows of tile ti, transposed [t][row]
-    __shared__ double sPj[CD_NB][CD_TT + 1];  // panel rows of tile tj
+    // sPi: panel rows of tile ti, [t][row]; sPj: of tile tj; sD (L_D, lower) lives in the
+    // sPj space while the diagonal block is factored; sDi = L_D^-1, zero padded to CD_NB
+    __shared__ __align__(16) double s_raw[2 * CD_NB * CD_PS + CD_NB * (CD_NB + 1)];
+    double(*sPi)[CD_PS] = reinterpret_cast<double(*)[CD_PS]>(s_raw);
+    double(*sPj)[CD_PS] = reinterpret_cast<double(*)[CD_PS]>(s_raw + CD_NB * CD_PS);
+    double(*sD)[CD_NB + 1] = reinterpret_cast<double(*)[CD_NB + 1]>(s_raw + CD_NB * CD_PS);
+    double(*sDi)[CD_NB + 1] = reinterpret_cast<double(*)[CD_NB + 1]>(s_raw + 2 * CD_NB * CD_PS);
     __shared__ int s_bad;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g8 = lane >> 2, t4 = lane & 3;
     if (tid == 0) s_bad = 0;
     for (int k0 = 0; k0 < m; k0 += CD_NB) {
         const int kb = min(CD_NB, m - k0);
-        // (a) factor the diagonal block (one warp, unblocked, in shared memory)
-        for (int idx = tid; idx < kb * kb; idx += CD_THREADS) {
-            const int i = idx / kb, j = idx - i * kb;
-            sD[i][j] = j <= i ? W[(long long)(k0 + i) * Mt + k0 + j] : 0.0;
+        // (a) diagonal block
+        for (int idx = tid; idx < CD_NB * CD_NB; idx += CD_THREADS) {
+            const int i = idx / CD_NB, j = idx - i * CD_NB;
+            sD[i][j] = (i < kb && j <= i) ? W[(long long)(k0 + i) * Mt + k0 + j] : 0.0;
         }
         __syncthreads();
         if (warp == 0) {
             for (int j = 0; j < kb; ++j) {
                 const double d = sD[j][j];
-                if (!(d > 0.0)) {
-                    if (lane == 0) s_bad = 1;
-                }
+                if (!(d > 0.0) && lane == 0) s_bad = 1;
                 const double ljj = sqrt(fmax(d, 1e-300));
                 __syncwarp();
                 if (lane == 0) sD[j][j] = ljj;
@@ -194,21 +208,31 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                 }
                 __syncwarp();
             }
+            // column `lane` of L_D^-1 by forward substitution
+            const int j = lane;
+            for (int i = 0; i < CD_NB; ++i) {
+                double x = 0.0;
+                if (i < kb && j < kb && i >= j) {
+                    if (i == j) {
+                        x = 1.0 / sD[j][j];
+                    } else {
+                        double sum = 0.0;
+                        for (int t = j; t < i; ++t) sum = fma(sD[i][t], sDi[t][j], sum);
+                        x = -sum / sD[i][i];
+                    }
+                }
+                sDi[i][j] = x;
+            }
         }
         __syncthreads();
         for (int idx = tid; idx < kb * kb; idx += CD_THREADS) {
             const int i = idx / kb, j = idx - i * kb;
             if (j <= i) W[(long long)(k0 + i) * Mt + k0 + j] = sD[i][j];
         }
-        // (b) + (c), one 64-row tile ti of the panel at a time: solve the tile's panel
-        // rows x <- x L_D^-T in shared memory (forward substitution, one thread per row),
-        // write them back, then apply the trailing update of the lower triangle
-        //   W[i][j] -= sum_t P[i][t] P[j][t],  i in tile ti, j in tiles tj <= ti
-        // (tiles tj < ti were solved by earlier passes).
+        __syncthreads();  // sD (aliasing sPj) is dead from here on
         const int r0 = k0 + kb;
         const int R = Mt - r0;
         const int nt = (R + CD_TT - 1) / CD_TT;
-        const int ty = tid / 16, tx = tid % 16;  // 4x4 micro-tile at rows 4 ty, cols 4 tx
         for (int ti = 0; ti < nt; ++ti) {
             const int ib = r0 + ti * CD_TT;
             for (int idx = tid; idx < CD_TT * CD_NB; idx += CD_THREADS) {
@@ -216,11 +240,23 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                 sPi[t][rr] = (t < kb && ib + rr < Mt) ? W[(long long)(ib + rr) * Mt + k0 + t] : 0.0;
             }
             __syncthreads();
-            if (tid < CD_TT && ib + tid < Mt) {
-                for (int j = 0; j < kb; ++j) {
-                    double x = sPi[j][tid];
-                    for (int t = 0; t < j; ++t) x = fma(-sPi[t][tid], sD[j][t], x);
-                    sPi[j][tid] = x / sD[j][j];
+            // (b) X = P L_D^-T: warp w owns rows 8w..8w+7 of the tile (in place)
+            {
+                double acc[4][2];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < CD_NB / 4; ++ks) {
+                    const int t = 4 * ks + t4;
+                    const double a = sPi[t][8 * warp + g8];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) cd_dmma(acc[q][0], acc[q][1], a, sDi[8 * q + g8][t]);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    sPi[8 * q + 2 * t4][8 * warp + g8] = acc[q][0];
+                    sPi[8 * q + 2 * t4 + 1][8 * warp + g8] = acc[q][1];
                 }
             }
             __syncthreads();
@@ -228,6 +264,8 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                 const int rr = idx / CD_NB, t = idx - rr * CD_NB;
                 if (t < kb && ib + rr < Mt) W[(long long)(ib + rr) * Mt + k0 + t] = sPi[t][rr];
             }
+            // (c) trailing update, warp w: rows 16 (w >> 1) .. +16, columns 32 (w & 1) .. +32
+            const int rb = warp >> 1, cb = warp & 1;
             for (int tj = 0; tj <= ti; ++tj) {
                 const int jb = r0 + tj * CD_TT;
                 if (tj < ti) {
@@ -237,31 +275,39 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                     }
                 }
                 __syncthreads();
-                const double(*Pj)[CD_TT + 1] = tj < ti ? sPj : sPi;
-                double acc[4][4];
+                double(*Pj)[CD_PS] = tj < ti ? sPj : sPi;
+                // skip warp tiles entirely above the diagonal of a diagonal tile
+                const bool live = !(tj == ti && 32 * cb > 16 * rb + 15);
+                if (live) {
+                    double acc[2][4][2];
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < 2; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-                for (int t = 0; t < kb; ++t) {
-                    double pi[4], pj[4];
+                        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) pi[a] = sPi[t][4 * ty + a];
+                    for (int ks = 0; ks < CD_NB / 4; ++ks) {
+                        const int t = 4 * ks + t4;
+                        double av[2], bv[4];
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) pj[b] = Pj[t][4 * tx + b];
+                        for (int a = 0; a < 2; ++a) av[a] = sPi[t][16 * rb + 8 * a + g8];
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
+                        for (int b = 0; b < 4; ++b) bv[b] = Pj[t][32 * cb + 8 * b + g8];
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) acc[a][b] = fma(pi[a], pj[b], acc[a][b]);
-                }
+                        for (int a = 0; a < 2; ++a)
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    const int i = ib + 4 * ty + a;
-                    if (i >= Mt) continue;
+                            for (int b = 0; b < 4; ++b) cd_dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+                    }
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int j = jb + 4 * tx + b;
-                        if (j <= i) W[(long long)i * Mt + j] -= acc[a][b];
+                    for (int a = 0; a < 2; ++a) {
+                        const int i = ib + 16 * rb + 8 * a + g8;
+                        if (i >= Mt) continue;
+                        double *Wi = W + (long long)i * Mt;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int j = jb + 32 * cb + 8 * b + 2 * t4;
+                            if (j <= i) Wi[j] -= acc[a][b][0];
+                            if (j + 1 <= i) Wi[j + 1] -= acc[a][b][1];
+                        }
                     }
                 }
                 __syncthreads();
@@ -321,7 +367,7 @@ int hxg_graph_assemble(int pr, int E, const double *g_h1, const double *g_hdiv, 
     if (E == 0) return HXG_OK;
     const int q = pr + 1, mw = q * q * q, mv = 3 * q * pr * pr;
     const long long M2 = 2LL * (mw + mv);
-    graph_assemble_kernel<<<grid_for((long long)E * M2 * M2, 256), 256, 0, (cudaStream_t)stream>>>(
+    graph_assemble_kernel<<<grid_for((long long)E * M2 * 32, 256), 256, 0, (cudaStream_t)stream>>>(
         mw, mv, E, g_h1, g_hdiv, S, full, packed);
     return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
 }
