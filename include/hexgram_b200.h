@@ -170,6 +170,26 @@ int hxg_condense_batched(int m, int n, int E, const double *G, const double *B, 
                          double *A, double *rhs, int *status, void *workspace, size_t workspace_bytes,
                          void *stream);
 
+/* Workspace (bytes) of hxg_acoustics_batched: per-point geometry fields. */
+size_t hxg_acoustics_workspace_size(int p0, int pr, int L, int E);
+
+/* dpg.py:234-277 _acoustics_b_tensorized (+ _kernels.py:1861-1936
+ * mixed_tens_term) and dpg.py:280-302 _acoustics_load, batched: the
+ * ultraweak-acoustics stiffness of E elements, trial order p0 (pressure + 3
+ * velocity components, each p0^3 L2 functions, n = 4 p0^3 columns), test
+ * order pr (H1 then H(div) rows, m = (pr+1)^3 + 3 pr^2 (pr+1)), L-point rule
+ * (tables from hxg_make_tables(L)).
+ *   Bre, Bim : [E][m][n] real / imaginary parts (row-major), required
+ *   B2       : [E][2m][2n] real block form [[Bre, -Bim], [Bim, Bre]] or NULL
+ *   fgrid    : [E][L^3] source sampled at the tensor nodes (l, m, n), or NULL
+ *   lre      : [E][2m] load in real block form [l_re; 0], or NULL
+ *   pairing  : 0 velocity (the printed form), 1 pressure (dpg.py:83-90)
+ *   status   : [E] or NULL, bit 0: det J <= 0 at a quadrature point */
+int hxg_acoustics_batched(int p0, int pr, double omega, int L, int E, const int *kind,
+                          const double *params, const double *tables, const double *fgrid, int pairing,
+                          double *Bre, double *Bim, double *B2, double *lre, int *status,
+                          void *workspace, size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -218,3 +218,97 @@ def condense(G: np.ndarray, B: np.ndarray, l: np.ndarray):
     X = solve_triangular(Lc.T, solve_triangular(Lc, B, lower=True), lower=False)
     y = solve_triangular(Lc.T, solve_triangular(Lc, l, lower=True), lower=False)
     return B.T @ X, B.T @ y
+
+
+def mixed_tens_term(p0, pr, su, sh, geom_code, gr, gc, nodes, wts, kind, par):
+    """_kernels.py:1861-1932 mixed_tens_term (numpy restatement, same stage
+    order xi3 -> xi2 -> xi1): out[i_flat, k_flat] = integral of
+    prod_d chi^(su_d)_{i_d+sh_d}(xi_d) nu_{k_d}(xi_d) g(xi), g by geom_code
+    (0: 1, 1: 1/detJ, 2: J[gr,gc]/detJ, 3: Jinv[gr,gc])."""
+    L = nodes.shape[0]
+    n = [pr + 1 - s for s in sh]
+    tab = []
+    for l in range(L):
+        c, d = shape1_h1(nodes[l], pr)
+        nu = shape1_l2(nodes[l], p0)
+        tab.append((c, d, nu))
+    g = np.empty((L, L, L))
+    for l in range(L):
+        for m in range(L):
+            for k in range(L):
+                J, Ji, det = geom_full(kind, par, (nodes[l], nodes[m], nodes[k]))
+                g[l, m, k] = (1.0, 1.0 / det, J[gr, gc] / det, Ji[gr, gc])[geom_code]
+    U = []  # U[d][i, k, node] = chi^(su)_{i+sh}(x) nu_k(x) w(x)
+    for dd in range(3):
+        Ud = np.empty((n[dd], p0, L))
+        for l in range(L):
+            c, d, nu = tab[l]
+            f = d if su[dd] == 1 else c
+            Ud[:, :, l] = np.outer(f[sh[dd]:sh[dd] + n[dd]], nu) * wts[l]
+        U.append(Ud)
+    gA = np.einsum("lmn,ckn->lmck", g, U[2])           # xi3
+    gB = np.einsum("lmck,bjm->lbjck", gA, U[1])        # xi2
+    out = np.einsum("lbjck,ail->abcijk", gB, U[0])     # xi1: [i1, i2, i3, k1, k2, k3]
+    nt = n[0] * n[1] * n[2]
+    # flat indices: i1 + n1 (i2 + n2 i3), k1 + p0 (k2 + p0 k3)
+    return out.transpose(2, 1, 0, 5, 4, 3).reshape(nt, p0 ** 3)
+
+
+def acoustics_stiffness(p0, pr, omega, kind, par):
+    """dpg.py:234-277 _acoustics_b_tensorized: (Bre, Bim) with the L = pr + 1 rule."""
+    nodes, wts = gauss_rule(pr + 1)
+    mw = (pr + 1) ** 3
+    mv = dim("Hdiv", (pr, pr, pr))
+    ny = p0 ** 3
+    Bre = np.zeros((mw + mv, 4 * ny))
+    Bim = np.zeros((mw + mv, 4 * ny))
+    T = lambda su, sh, gc, r, c: mixed_tens_term(p0, pr, su, sh, gc, r, c, nodes, wts, kind, par)  # noqa: E731
+    Bim[:mw, :ny] += omega * T((0, 0, 0), (0, 0, 0), 0, 0, 0)
+    for d in range(3):
+        su = tuple(1 if e == d else 0 for e in range(3))
+        for c in range(3):
+            Bre[:mw, ny * (1 + c):ny * (2 + c)] -= T(su, (0, 0, 0), 3, d, c)
+    off = mw
+    for a in range(3):
+        sh = tuple(0 if e == a else 1 for e in range(3))
+        na = (pr + 1 - sh[0]) * (pr + 1 - sh[1]) * (pr + 1 - sh[2])
+        Bre[off:off + na, :ny] -= T((1, 1, 1), sh, 1, 0, 0)
+        su = tuple(0 if e == a else 1 for e in range(3))
+        for c in range(3):
+            Bim[off:off + na, ny * (1 + c):ny * (2 + c)] += omega * T(su, sh, 2, c, a)
+        off += na
+    return Bre, Bim
+
+
+def acoustics_load(p0, pr, kind, par, fgrid, pairing="velocity"):
+    """dpg.py:280-302 _acoustics_load (real part over the stacked test space);
+    fgrid = the source at the tensor nodes (l, m, n) of the L = pr + 1 rule."""
+    L = pr + 1
+    nodes, wts = gauss_rule(L)
+    q = pr + 1
+    mw = q ** 3
+    nb = q * pr * pr
+    lre = np.zeros(mw + 3 * nb)
+    if fgrid is None:
+        return lre
+    fg = np.asarray(fgrid).reshape(L, L, L)
+    C = [shape1_h1(x, pr)[0] for x in nodes]
+    NU = [shape1_l2(x, pr)[:pr] for x in nodes]
+    for l in range(L):
+        for m in range(L):
+            for k in range(L):
+                J, _, det = geom_full(kind, par, (nodes[l], nodes[m], nodes[k]))
+                w = wts[l] * wts[m] * wts[k] * fg[l, m, k]
+                pts = (l, m, k)
+                if pairing == "pressure":
+                    phi = np.einsum("i,j,k->kji", C[l], C[m], C[k]).reshape(-1)
+                    lre[:mw] += phi * (w * det)
+                else:
+                    Jrows = J.sum(axis=0)
+                    off = mw
+                    for a in range(3):
+                        f = [C[pts[d]] if d == a else NU[pts[d]] for d in range(3)]
+                        v = np.einsum("i,j,k->kji", f[0], f[1], f[2]).reshape(-1)
+                        lre[off:off + nb] += w * Jrows[a] * v
+                        off += nb
+    return lre

@@ -46,6 +46,8 @@ EXPORTED = (
     "hxg_graph_assemble",
     "hxg_condense_workspace_size",
     "hxg_condense_batched",
+    "hxg_acoustics_workspace_size",
+    "hxg_acoustics_batched",
 )
 
 _lib = None
@@ -105,6 +107,11 @@ def lib():
     L.hxg_condense_workspace_size.restype = _sz
     L.hxg_condense_batched.argtypes = [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     L.hxg_condense_batched.restype = _i
+    L.hxg_acoustics_workspace_size.argtypes = [_i, _i, _i, _i]
+    L.hxg_acoustics_workspace_size.restype = _sz
+    L.hxg_acoustics_batched.argtypes = [_i, _i, ctypes.c_double, _i, _i, _vp, _vp, _vp, _vp, _i,
+                                        _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    L.hxg_acoustics_batched.restype = _i
     _lib = L
     return L
 

@@ -16,12 +16,17 @@
 //     (n+1) x (n+1) block is -B~^T G^-1 B~ = -[[A, rhs], [rhs^T, .]], so the
 //     Cholesky factor, both triangular solves of cho_solve and the two
 //     products B^T(.) are one right-looking blocked elimination
-//     (condense_kernel), FP64 throughout.
+//     (condense_kernel), FP64 throughout;
+//   * the sum-factorized ultraweak-acoustics stiffness B and load l
+//     (dpg.py:234-302, _kernels.py:1861-1936 mixed_tens_term): 16 output
+//     blocks of rectangular test x trial mixed terms, three-stage contraction
+//     (xi3, xi2, xi1) per block (acoustics_block_kernel).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 
 #include "../../include/hexgram_b200.h"
+#include "hxg_geom.cuh"
 #include "hxg_plan.h"
 
 using namespace hxg;
@@ -341,6 +346,238 @@ __global__ void condense_final_kernel(int m, int n, int Ec, const double *__rest
     }
 }
 
+// ---------------------------------------------------------------------------
+// ultraweak acoustics stiffness (dpg.py:234-277 _acoustics_b_tensorized) and load
+// (dpg.py:280-302 _acoustics_load)
+// ---------------------------------------------------------------------------
+// per-point geometry fields [E][AC_NF][L^3], point (l, m, n) -> (l L + m) L + n:
+//   0: 1, 1: 1/det, 2 + 3c + a: J[c][a]/det, 11 + 3d + c: Jinv[d][c]
+// (the g of mixed_tens_term, _kernels.py:1899-1907)
+constexpr int AC_NF = 20;
+
+__global__ void acoustics_geom_kernel(int L, int E, const int *__restrict__ kind,
+                                      const double *__restrict__ params, const double *__restrict__ tab,
+                                      double *__restrict__ F, int *__restrict__ status)
+{
+    const int L3 = L * L * L;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)E * L3;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int e = (int)(idx / L3), pt = (int)(idx - (long long)e * L3);
+        const int l = pt / (L * L), m = (pt / L) % L, n = pt % L;
+        double J[3][3];
+        dev_jacobian(kind[e], params + 24LL * e, tab[TAB_NODES + l], tab[TAB_NODES + m], tab[TAB_NODES + n], J);
+        const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+        const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+        const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+        const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+        const double inv = 1.0 / det;
+        double Ji[3][3];
+        Ji[0][0] = c00 * inv;
+        Ji[1][0] = c01 * inv;
+        Ji[2][0] = c02 * inv;
+        Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * inv;
+        Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * inv;
+        Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * inv;
+        Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * inv;
+        Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * inv;
+        Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * inv;
+        double *f = F + (long long)e * AC_NF * L3 + pt;
+        f[0] = 1.0;
+        f[(long long)1 * L3] = 1.0 / det;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                f[(long long)(2 + 3 * c + a) * L3] = J[c][a] / det;
+                f[(long long)(11 + 3 * c + a) * L3] = Ji[c][a];
+            }
+        if (!(det > 0.0) && status) atomicOr(status + e, 1);
+    }
+}
+
+struct AcTerm {
+    int su[3], sh[3], field;
+    double scale;
+};
+struct AcBlock {
+    int nterm, re;  // re: 1 -> Bre, 0 -> Bim
+    int row_off, col_blk, a;  // a: H(div) component of the test rows (-1: H1 rows)
+    AcTerm t[3];
+};
+
+// block b of the 16 (dpg.py:240-276, in its order); omega folded into scale
+__device__ AcBlock ac_block(int b, int pr, double omega)
+{
+    AcBlock B{};
+    const int q = pr + 1, mw = q * q * q, nb = q * pr * pr;
+    if (b == 0) {  // (i omega p, q): Bim[:mw, :ny] += omega T(0,0,0; g = 1)
+        B.nterm = 1; B.re = 0; B.row_off = 0; B.col_blk = 0; B.a = -1;
+        B.t[0] = AcTerm{{0, 0, 0}, {0, 0, 0}, 0, omega};
+    } else if (b <= 3) {  // -(u, grad q): Bre[:mw, ny(1+c)] -= sum_d T(e_d, 0; Jinv[d][c])
+        const int c = b - 1;
+        B.nterm = 3; B.re = 1; B.row_off = 0; B.col_blk = 1 + c; B.a = -1;
+        for (int d = 0; d < 3; ++d)
+            B.t[d] = AcTerm{{d == 0, d == 1, d == 2}, {0, 0, 0}, 11 + 3 * d + c, -1.0};
+    } else if (b <= 6) {  // -(p, div v): Bre[off_a, :ny] -= T(1,1,1; sh_a; 1/det)
+        const int a = b - 4;
+        B.nterm = 1; B.re = 1; B.row_off = mw + a * nb; B.col_blk = 0; B.a = a;
+        B.t[0] = AcTerm{{1, 1, 1}, {a != 0, a != 1, a != 2}, 1, -1.0};
+    } else {  // (i omega u, v): Bim[off_a, ny(1+c)] += omega T(su_a, sh_a; J[c][a]/det)
+        const int a = (b - 7) / 3, c = (b - 7) % 3;
+        B.nterm = 1; B.re = 0; B.row_off = mw + a * nb; B.col_blk = 1 + c; B.a = a;
+        B.t[0] = AcTerm{{a != 0, a != 1, a != 2}, {a != 0, a != 1, a != 2}, 2 + 3 * c + a, omega};
+    }
+    return B;
+}
+
+// One CTA per (block, element).  Per term: stage A (xi3) sA[l][m][i3][k3], stage B
+// (xi2) sBt[l][i2][k2][i3][k3], stage C (xi1) accumulated into the owner thread's
+// output entries (first term stores, later terms add).  Dynamic shared memory.
+__global__ void __launch_bounds__(256) acoustics_block_kernel(int p0, int pr, int L, double omega,
+                                                             const double *__restrict__ tab,
+                                                             const double *__restrict__ F,
+                                                             double *__restrict__ Bre,
+                                                             double *__restrict__ Bim)
+{
+    extern __shared__ double sm[];
+    const int b = blockIdx.x, e = blockIdx.y;
+    const AcBlock B = ac_block(b, pr, omega);
+    const int q = pr + 1, mw = q * q * q, mv = 3 * q * pr * pr, m = mw + mv;
+    const int ny = p0 * p0 * p0, n = 4 * ny;
+    const int L3 = L * L * L;
+    const int sh0 = B.t[0].sh[0], sh1 = B.t[0].sh[1], sh2 = B.t[0].sh[2];  // shared by a block's terms
+    const int n1 = q - sh0, n2 = q - sh1, n3 = q - sh2;
+    const int nt = n1 * n2 * n3;
+    // shared: 1D tables u[f][k][l] (f: chi, chi'), nu[k][l], w[l]; stage buffers
+    double *sU = sm;                       // [2][q + 1][L]
+    double *sNu = sU + 2 * (q + 1) * L;    // [p0][L]
+    double *sW = sNu + p0 * L;             // [L]
+    double *sA = sW + L;                   // [L][L][n3][p0]
+    double *sBt = sA + L * L * n3 * p0;    // [L][n2][p0][n3][p0]
+    for (int i = threadIdx.x; i < 2 * (q + 1) * L; i += blockDim.x) {
+        const int f = i / ((q + 1) * L), r = i - f * (q + 1) * L, k = r / L, l = r - k * L;
+        sU[i] = tab[TAB_T + (f * KT + k) * LT + l];
+    }
+    for (int i = threadIdx.x; i < p0 * L; i += blockDim.x) {
+        const int k = i / L, l = i - k * L;
+        sNu[i] = tab[TAB_T + (1 * KT + k + 1) * LT + l];  // nu_k = chi'_{k+1}
+    }
+    for (int i = threadIdx.x; i < L; i += blockDim.x) sW[i] = tab[TAB_WTS + i];
+    double *out = (B.re ? Bre : Bim) + (long long)e * m * n;
+    const double *Fe = F + (long long)e * AC_NF * L3;
+    for (int t = 0; t < B.nterm; ++t) {
+        const AcTerm T = B.t[t];
+        const double *g = Fe + (long long)T.field * L3;
+        const double *u1 = sU + (T.su[0] * (q + 1) + sh0) * L;
+        const double *u2 = sU + (T.su[1] * (q + 1) + sh1) * L;
+        const double *u3 = sU + (T.su[2] * (q + 1) + sh2) * L;
+        __syncthreads();  // tables ready / previous term's stage buffers consumed
+        // stage A: sum over n (xi3), _kernels.py:1908-1911
+        for (int i = threadIdx.x; i < L * L * n3 * p0; i += blockDim.x) {
+            const int lm = i / (n3 * p0), r = i - lm * (n3 * p0), i3 = r / p0, k3 = r - i3 * p0;
+            double s = 0.0;
+            for (int nn = 0; nn < L; ++nn)
+                s = fma(sW[nn] * g[lm * L + nn], u3[i3 * L + nn] * sNu[k3 * L + nn], s);
+            sA[i] = s;
+        }
+        __syncthreads();
+        // stage B: sum over m (xi2), _kernels.py:1912-1918
+        const int nb2 = n2 * p0 * n3 * p0;
+        for (int i = threadIdx.x; i < L * nb2; i += blockDim.x) {
+            const int l = i / nb2, r = i - l * nb2;
+            const int i2 = r / (p0 * n3 * p0), r2 = r - i2 * (p0 * n3 * p0);
+            const int k2 = r2 / (n3 * p0), r3 = r2 - k2 * (n3 * p0);  // r3 = i3 * p0 + k3
+            double s = 0.0;
+            for (int mm = 0; mm < L; ++mm)
+                s = fma(u2[i2 * L + mm] * sNu[k2 * L + mm] * sW[mm], sA[(l * L + mm) * n3 * p0 + r3], s);
+            sBt[i] = s;
+        }
+        __syncthreads();
+        // stage C: sum over l (xi1), _kernels.py:1919-1930; entry (i, k) of the block
+        for (int idx = threadIdx.x; idx < nt * ny; idx += blockDim.x) {
+            const int i = idx / ny, k = idx - i * ny;
+            const int i1 = i % n1, i2 = (i / n1) % n2, i3 = i / (n1 * n2);
+            const int k1 = k % p0, k2 = (k / p0) % p0, k3 = k / (p0 * p0);
+            const int r = ((i2 * p0 + k2) * n3 + i3) * p0 + k3;
+            double s = 0.0;
+            for (int l = 0; l < L; ++l) s = fma(u1[i1 * L + l] * sNu[k1 * L + l] * sW[l], sBt[l * nb2 + r], s);
+            double *o = out + (long long)(B.row_off + i) * n + B.col_blk * ny + k;
+            *o = (t == 0 ? 0.0 : *o) + T.scale * s;
+        }
+    }
+}
+
+// dpg.py:285-302: real part of the load over the stacked test space,
+// lre[e][:mw] (pressure pairing) or lre[e][mw:] (velocity pairing), other part 0.
+// fgrid [E][L^3]: the source sampled at the tensor nodes (point (l, m, n)).
+__global__ void acoustics_load_kernel(int pr, int L, int E, int pairing, const double *__restrict__ tab,
+                                      const double *__restrict__ F, const double *__restrict__ fgrid,
+                                      double *__restrict__ lre)
+{
+    const int q = pr + 1, mw = q * q * q, nb = q * pr * pr, m = mw + 3 * nb;
+    const int L3 = L * L * L;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)E * m;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int e = (int)(idx / m), i = (int)(idx - (long long)e * m);
+        const double *Fe = F + (long long)e * AC_NF * L3;
+        const double *fg = fgrid + (long long)e * L3;
+        double s = 0.0;
+        if (pairing == 1 && i < mw) {  // (f, q): w det f phi_i
+            const int i1 = i % q, i2 = (i / q) % q, i3 = i / (q * q);
+            for (int pt = 0; pt < L3; ++pt) {
+                const int l = pt / (L * L), mm = (pt / L) % L, nn = pt % L;
+                const double w = tab[TAB_WTS + l] * tab[TAB_WTS + mm] * tab[TAB_WTS + nn];
+                const double phi = tab[TAB_T + i1 * LT + l] * tab[TAB_T + i2 * LT + mm] * tab[TAB_T + i3 * LT + nn];
+                s += phi * (w * (1.0 / Fe[(long long)L3 + pt]) * fg[pt]);
+            }
+        } else if (pairing == 0 && i >= mw) {  // (f 1, J v_hat): w f sum_r J[r][a] v_a
+            const int a = (i - mw) / nb, x = (i - mw) - a * nb;
+            const int na0 = a == 0 ? q : pr, na1 = a == 1 ? q : pr;
+            const int xd[3] = {x % na0, (x / na0) % na1, x / (na0 * na1)};
+            for (int pt = 0; pt < L3; ++pt) {
+                const int p3[3] = {pt / (L * L), (pt / L) % L, pt % L};
+                const double w = tab[TAB_WTS + p3[0]] * tab[TAB_WTS + p3[1]] * tab[TAB_WTS + p3[2]];
+                double v = 1.0;
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                    v *= d == a ? tab[TAB_T + xd[d] * LT + p3[d]] : tab[TAB_T + (KT + xd[d] + 1) * LT + p3[d]];
+                const double det = 1.0 / Fe[(long long)L3 + pt];
+                double jr = 0.0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) jr += Fe[(long long)(2 + 3 * c + a) * L3 + pt] * det;
+                s += (w * fg[pt]) * jr * v;
+            }
+        }
+        lre[(long long)e * 2 * m + i] = s;
+        lre[(long long)e * 2 * m + m + i] = 0.0;
+    }
+}
+
+// real block form [[Bre, -Bim], [Bim, Bre]] (dpg.py:322-323)
+__global__ void block_form_kernel(int m, int n, int E, const double *__restrict__ Bre,
+                                  const double *__restrict__ Bim, double *__restrict__ B2)
+{
+    const long long per = 4LL * m * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)E * per;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long e = idx / per, rc = idx - e * per;
+        const int r = (int)(rc / (2 * n)), c = (int)(rc - (long long)r * 2 * n);
+        const int R = r < m ? r : r - m, C = c < n ? c : c - n;
+        const long long src = (e * m + R) * n + C;
+        double v;
+        if ((r < m) == (c < n)) v = Bre[src];
+        else v = r < m ? -Bim[src] : Bim[src];
+        B2[idx] = v;
+    }
+}
+
+size_t ac_smem_bytes(int p0, int pr, int L)
+{
+    const int q = pr + 1;
+    return sizeof(double) * ((size_t)2 * (q + 1) * L + (size_t)p0 * L + L + (size_t)L * L * q * p0 +
+                             (size_t)L * q * p0 * q * p0);
+}
+
 int grid_for(long long work, int threads)
 {
     return (int)std::max<long long>(1, std::min<long long>((work + threads - 1) / threads, 148LL * 16));
@@ -404,6 +641,46 @@ int hxg_condense_batched(int m, int n, int E, const double *G, const double *B, 
         condense_final_kernel<<<grid_for((long long)Ec * n * n, 256), 256, 0, st>>>(
             m, n, Ec, W, A + (long long)e0 * n * n, rhs ? rhs + (long long)e0 * n : nullptr);
     }
+    return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
+}
+
+size_t hxg_acoustics_workspace_size(int p0, int pr, int L, int E)
+{
+    if (p0 < 1 || pr < 1 || L < 1 || E < 0) return 0;
+    return sizeof(double) * (size_t)E * AC_NF * L * L * L;
+}
+
+int hxg_acoustics_batched(int p0, int pr, double omega, int L, int E, const int *kind,
+                          const double *params, const double *tables, const double *fgrid, int pairing,
+                          double *Bre, double *Bim, double *B2, double *lre, int *status,
+                          void *workspace, size_t ws_bytes, void *stream)
+{
+    if (p0 < 1 || pr < p0 || pr + 2 > KT || L < 1 || L > LT) return HXG_ERR_ORDER;
+    if (E < 0 || pairing < 0 || pairing > 1) return HXG_ERR_ARG;
+    if (E == 0) return HXG_OK;
+    if (!kind || !params || !tables || !Bre || !Bim || (lre && !fgrid)) return HXG_ERR_ARG;
+    if (!workspace || ws_bytes < hxg_acoustics_workspace_size(p0, pr, L, E)) return HXG_ERR_WORKSPACE;
+    const size_t smem = ac_smem_bytes(p0, pr, L);
+    if (smem > 227 * 1024) return HXG_ERR_ORDER;
+    cudaStream_t st = (cudaStream_t)stream;
+    double *F = (double *)workspace;
+    if (status && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
+    acoustics_geom_kernel<<<grid_for((long long)E * L * L * L, 256), 256, 0, st>>>(L, E, kind, params, tables,
+                                                                                  F, status);
+    const int q = pr + 1, m = q * q * q + 3 * q * pr * pr, n = 4 * p0 * p0 * p0;
+    // blocks no term writes (Bre[:mw, :ny], Bim[:mw, ny:], ...) are zero
+    if (cudaMemsetAsync(Bre, 0, sizeof(double) * (size_t)E * m * n, st) != cudaSuccess ||
+        cudaMemsetAsync(Bim, 0, sizeof(double) * (size_t)E * m * n, st) != cudaSuccess)
+        return HXG_ERR_CUDA;
+    if (cudaFuncSetAttribute(acoustics_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return HXG_ERR_CUDA;
+    acoustics_block_kernel<<<dim3(16, E), 256, smem, st>>>(p0, pr, L, omega, tables, F, Bre, Bim);
+    if (B2)
+        block_form_kernel<<<grid_for(4LL * E * m * n, 256), 256, 0, st>>>(m, n, E, Bre, Bim, B2);
+    if (lre)
+        acoustics_load_kernel<<<grid_for((long long)E * m, 128), 128, 0, st>>>(pr, L, E, pairing, tables, F,
+                                                                             fgrid, lre);
     return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
 }
 

@@ -9,7 +9,11 @@ rows 2 and 3):
   block form [[re, -im], [im, re]] (dpg.py:205-219, ``hxg_graph_assemble``);
 * ``condense`` (dpg.py:348-357) -- static condensation A = B^T G^-1 B,
   rhs = B^T G^-1 l through a Cholesky factorisation of G
-  (``hxg_condense_batched``).
+  (``hxg_condense_batched``);
+* ``acoustics_ultraweak_element`` (dpg.py:305-336) -- the ultraweak
+  acoustics element system: G from the adjoint-graph Gram, the
+  sum-factorized stiffness B (dpg.py:234-277, mixed_tens_term) and the load
+  l (dpg.py:280-302) in real block form (``hxg_acoustics_batched``).
 
 The per-element functions keep the reference's names, arguments, errors and
 return types; the ``*_batched`` functions are the native entries (device
@@ -18,16 +22,21 @@ sm_100a kernels of libhexgram_b200.so; there is no CPU fallback.
 """
 
 import ctypes
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from .errors import NonSPDError, SimplificationNotApplicableError
-from .geometry import ElementMap, classify
+from .geometry import ElementMap, classify, map_position
 from .gram import GramResult, OpCounters, counters
 from .spaces import SpaceSignature, dim
 
 __all__ = [
+    "DpgElementSystem",
+    "UltraweakAcousticsProblem",
+    "acoustics_ultraweak_element",
+    "acoustics_batched",
     "graph_mixed_block",
     "adjoint_graph_gram",
     "adjoint_graph_gram_batched",
@@ -196,3 +205,125 @@ def condense(system):
     rhs = rhs[0].cpu().numpy()
     system.condensed = (A, rhs)
     return A, rhs
+
+
+# ---------------------------------------------------------------------------
+# ultraweak acoustics element system (dpg.py:44-92, 234-336)
+# ---------------------------------------------------------------------------
+@dataclass
+class DpgElementSystem:
+    """Arrays of the enriched element system G s - B u = -l (dpg.py:44-75)."""
+
+    G: np.ndarray
+    B: np.ndarray
+    l: np.ndarray
+    orders: tuple
+    is_complex: bool = False
+    condensed: tuple | None = None
+    gram_counters: OpCounters | None = None
+
+    def __post_init__(self):
+        m = self.B.shape[0]
+        n = self.B.shape[1]
+        if self.is_complex:
+            m //= 2
+            n //= 2
+        if m <= n:
+            raise ValueError(f"enriched test space must dominate: m={m} <= n={n}")
+
+    @property
+    def m(self) -> int:
+        return self.B.shape[0] // (2 if self.is_complex else 1)
+
+    @property
+    def n(self) -> int:
+        return self.B.shape[1] // (2 if self.is_complex else 1)
+
+
+@dataclass(frozen=True)
+class UltraweakAcousticsProblem:
+    """Frequency, broken-norm correction and source (dpg.py:78-92)."""
+
+    omega: float
+    alpha: float
+    f: object = None
+    load_pairing: str = "velocity"
+
+    def __post_init__(self):
+        if self.omega <= 0:
+            raise ValueError("omega must be positive")
+        if self.alpha <= 0:
+            raise ValueError("alpha must be positive")
+        if self.load_pairing not in ("velocity", "pressure"):
+            raise ValueError("load_pairing must be 'velocity' or 'pressure'")
+
+
+def acoustics_batched(p0: int, pr: int, omega: float, kind, params, fgrid=None, *,
+                      pairing: str = "velocity", block_form: bool = True, device=None, stream=None):
+    """Batched ultraweak-acoustics stiffness (dpg.py:234-277) and load
+    (dpg.py:280-302) on the device, rule L = pr + 1.  kind int32 [E], params
+    float64 [E, 24]; fgrid float64 [E, L^3] (source at the tensor nodes, point
+    (l, m, n) -> (l L + m) L + n) or None.  Returns (Bre [E, m, n],
+    Bim [E, m, n], B2 [E, 2m, 2n] or None, l [E, 2m] or None, status)."""
+    from .engine import _check
+
+    eng = _engine(device)
+    st, sp = _stream(eng, stream)
+    dev = eng.device
+    L = pr + 1
+    kind = torch.as_tensor(kind, dtype=torch.int32).to(dev).contiguous()
+    E = int(kind.shape[0])
+    params = torch.as_tensor(params, dtype=torch.float64).to(dev).reshape(E, 24).contiguous()
+    q = pr + 1
+    m = q ** 3 + 3 * pr * pr * q
+    n = 4 * p0 ** 3
+    Bre = torch.empty((E, m, n), dtype=torch.float64, device=dev)
+    Bim = torch.empty((E, m, n), dtype=torch.float64, device=dev)
+    B2 = torch.empty((E, 2 * m, 2 * n), dtype=torch.float64, device=dev) if block_form else None
+    lre = None
+    if fgrid is not None:
+        fgrid = torch.as_tensor(fgrid, dtype=torch.float64).to(dev).reshape(E, L ** 3).contiguous()
+        lre = torch.empty((E, 2 * m), dtype=torch.float64, device=dev)
+    status = torch.zeros(E, dtype=torch.int32, device=dev)
+    tab = eng.tables(L, stream=st)
+    ws_bytes = eng.lib.hxg_acoustics_workspace_size(p0, pr, L, E)
+    ws = eng.workspace(ws_bytes)
+    rc = eng.lib.hxg_acoustics_batched(p0, pr, float(omega), L, E, _vp(kind), _vp(params), _vp(tab),
+                                       _vp(fgrid), 0 if pairing == "velocity" else 1, _vp(Bre),
+                                       _vp(Bim), _vp(B2), _vp(lre), _vp(status), _vp(ws), ws_bytes, sp)
+    _check(rc, "hxg_acoustics_batched")
+    return Bre, Bim, B2, lre, status
+
+
+def _source_grid(fun, emap: ElementMap, L: int) -> np.ndarray | None:
+    """The source sampled at the tensor nodes, as dpg.py:95-103 does on the host."""
+    if fun is None:
+        return None
+    from .quadrature import tensor_rule
+
+    pts = tensor_rule(L).points
+    if np.isscalar(fun):
+        return np.full(pts.shape[0], float(fun))
+    return np.array([float(fun(map_position(emap, p))) for p in pts])
+
+
+def acoustics_ultraweak_element(problem: UltraweakAcousticsProblem, p0: int, dp: int,
+                                emap: ElementMap, backend: str = "tensorized") -> DpgElementSystem:
+    """Ultraweak acoustics element arrays in real block form (dpg.py:305-336),
+    on the device: G = adjoint_graph_gram(pr, omega, alpha, emap, backend), B
+    by sum factorization (both the reference's routes give the same integral),
+    l from the source sampled at the tensor nodes."""
+    if p0 < 1 or dp < 1:
+        raise ValueError("p0 and dp must be >= 1")
+    pr = p0 + dp
+    L = pr + 1
+    gres = adjoint_graph_gram(pr, problem.omega, problem.alpha, emap, backend)
+    fg = _source_grid(problem.f, emap, L)
+    _, _, B2, lre, status = acoustics_batched(
+        p0, pr, problem.omega, np.array([emap.kind_code], np.int32), emap.params.reshape(1, 24),
+        None if fg is None else fg[None], pairing=problem.load_pairing)
+    B = B2[0].cpu().numpy()
+    m = B.shape[0] // 2
+    l = lre[0].cpu().numpy() if lre is not None else np.zeros(2 * m)
+    return DpgElementSystem(G=gres.matrix, B=B, l=l, orders=(p0, dp, pr), is_complex=True,
+                            gram_counters=gres.counters)

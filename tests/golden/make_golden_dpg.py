@@ -87,8 +87,24 @@ def main():
             d[key + "_A"], d[key + "_rhs"] = A, rhs
             ccases.append(key)
     d["condense_cases"] = np.array(ccases)
+    # ultraweak acoustics stiffness + load (dpg.py:234-336): B (real block form), l
+    acases = []
+    for pairing in ("velocity", "pressure"):
+        prob = dpg.UltraweakAcousticsProblem(omega=1.7, alpha=0.3, f=source, load_pairing=pairing)
+        for p0, dp in ((1, 1), (2, 1), (1, 2), (2, 2)):
+            for name in ("identity", "affine", "trilinear", "extrusion"):
+                if pairing == "pressure" and name != "trilinear":
+                    continue
+                sys_ = dpg.acoustics_ultraweak_element(prob, p0, dp, maps[name], "tensorized")
+                key = f"ac_{pairing}_{p0}_{dp}_{name}"
+                d[key + "_B"], d[key + "_l"] = sys_.B, sys_.l
+                if p0 == 1 and dp == 1:
+                    d[key + "_G"] = sys_.G
+                acases.append(key)
+    d["acoustics_cases"] = np.array(acases)
     np.savez_compressed(OUT, **d)
-    print("wrote", OUT, len(cases), "graph cases,", len(ccases), "condensation cases")
+    print("wrote", OUT, len(cases), "graph cases,", len(ccases), "condensation cases,",
+          len(acases), "acoustics cases")
 
 
 if __name__ == "__main__":

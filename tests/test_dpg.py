@@ -1,5 +1,7 @@
-"""SURVEY 8(f) rows 2-3: the adjoint-graph Gram (dpg.py:179-231, cross block
-dpg.py:155-176) and batched static condensation (dpg.py:348-357).
+"""SURVEY 8(f) rows 2-4: the adjoint-graph Gram (dpg.py:179-231, cross block
+dpg.py:155-176), batched static condensation (dpg.py:348-357) and the
+sum-factorized ultraweak-acoustics stiffness and load (dpg.py:234-336,
+_kernels.py:1861-1936).
 
 CPU tests pin the numpy oracle (oracle/oracle.py) to the reference's own
 outputs (tests/golden/golden_dpg.npz, written by make_golden_dpg.py).  GPU
@@ -226,3 +228,107 @@ def test_condense_not_spd_and_edge_cases():
     # no load vector: rhs = 0
     A, rhs, _ = condense_batched(G[:1, iu[0], iu[1]], B[:1], None)
     assert torch.count_nonzero(rhs) == 0
+
+
+# --------------------------------------------------------------------------- row 4
+def _src(x):
+    return np.sin(3.0 * x[0]) + x[1] * x[2] + 0.5
+
+
+def _ac_case(gd, key):
+    _, pairing, p0, dp, name = str(key).split("_")
+    return pairing, int(p0), int(dp), name, int(gd[f"map_{name}_kind"]), gd[f"map_{name}_params"]
+
+
+def _fgrid(kind, par, L):
+    from paper_1711_00984_b200.geometry import KIND_NAMES, ElementMap, map_position
+    from paper_1711_00984_b200.quadrature import tensor_rule
+
+    em = ElementMap(KIND_NAMES[kind], par)
+    return np.array([_src(map_position(em, p)) for p in tensor_rule(L).points])
+
+
+def test_oracle_acoustics_golden(gd, orc):
+    for key in gd["acoustics_cases"]:
+        pairing, p0, dp, name, kind, par = _ac_case(gd, key)
+        pr = p0 + dp
+        Bre, Bim = orc.acoustics_stiffness(p0, pr, 1.7, kind, par)
+        assert rel(np.block([[Bre, -Bim], [Bim, Bre]]), gd[key + "_B"]) <= 1e-14, key
+        lre = orc.acoustics_load(p0, pr, kind, par, _fgrid(kind, par, pr + 1), pairing)
+        assert rel(np.concatenate([lre, 0 * lre]), gd[key + "_l"]) <= 1e-14, key
+
+
+@pytest.mark.gpu
+def test_acoustics_element_golden(gd):
+    from paper_1711_00984_b200.dpg import UltraweakAcousticsProblem, acoustics_ultraweak_element
+    from paper_1711_00984_b200.geometry import KIND_NAMES, ElementMap
+
+    for key in gd["acoustics_cases"]:
+        pairing, p0, dp, name, kind, par = _ac_case(gd, key)
+        prob = UltraweakAcousticsProblem(omega=1.7, alpha=0.3, f=_src, load_pairing=pairing)
+        s = acoustics_ultraweak_element(prob, p0, dp, ElementMap(KIND_NAMES[kind], par), "tensorized")
+        assert s.is_complex and s.orders == (p0, dp, p0 + dp)
+        assert s.B.shape == gd[key + "_B"].shape
+        assert rel(s.B, gd[key + "_B"]) <= TOL, key
+        assert rel(s.l, gd[key + "_l"]) <= TOL, key
+        if (key + "_G") in gd.files:
+            assert rel(s.G, gd[key + "_G"]) <= TOL, key
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p0,pr", [(1, 2), (2, 4), (3, 5), (4, 7)])
+def test_acoustics_batched_vs_oracle(p0, pr, orc):
+    from paper_1711_00984_b200.dpg import acoustics_batched
+    from paper_1711_00984_b200.inputs import trilinear_batch
+
+    E = 4
+    b = trilinear_batch(E, 40 + pr)
+    L = pr + 1
+    fg = np.stack([_fgrid(int(b.kind[e]), b.params[e], L) for e in range(E)])
+    Bre, Bim, B2, lre, st = acoustics_batched(p0, pr, 0.9, b.kind, b.params, fg)
+    Bre, Bim, B2, lre = (t.cpu().numpy() for t in (Bre, Bim, B2, lre))
+    assert int(st.abs().sum()) == 0
+    for e in range(E):
+        Rre, Rim = orc.acoustics_stiffness(p0, pr, 0.9, int(b.kind[e]), b.params[e])
+        assert rel(Bre[e], Rre) <= TOL and rel(Bim[e], Rim) <= TOL
+        assert np.array_equal(B2[e], np.block([[Bre[e], -Bim[e]], [Bim[e], Bre[e]]]))
+        rl = orc.acoustics_load(p0, pr, int(b.kind[e]), b.params[e], fg[e], "velocity")
+        assert rel(lre[e], np.concatenate([rl, 0 * rl])) <= TOL
+
+
+@pytest.mark.gpu
+def test_acoustics_full_pipeline_condense(orc):
+    """G (graph Gram, packed) and B from the device feed the device condensation;
+    compared with the oracle condensation of the oracle's G and B."""
+    from paper_1711_00984_b200.dpg import acoustics_batched, adjoint_graph_gram_batched, condense_batched
+    from paper_1711_00984_b200.inputs import trilinear_batch
+
+    p0, pr, E = 2, 3, 3
+    b = trilinear_batch(E, 77)
+    L = pr + 1
+    fg = np.stack([_fgrid(int(b.kind[e]), b.params[e], L) for e in range(E)])
+    Gp = adjoint_graph_gram_batched(pr, 1.3, 0.4, b.kind, b.params)
+    _, _, B2, l2, _ = acoustics_batched(p0, pr, 1.3, b.kind, b.params, fg)
+    A, rhs, _ = condense_batched(Gp, B2, l2)
+    for e in range(E):
+        G = orc.adjoint_graph_gram(pr, 1.3, 0.4, "general", int(b.kind[e]), b.params[e])
+        Rre, Rim = orc.acoustics_stiffness(p0, pr, 1.3, int(b.kind[e]), b.params[e])
+        rl = orc.acoustics_load(p0, pr, int(b.kind[e]), b.params[e], fg[e], "velocity")
+        Ar, rr = orc.condense(G, np.block([[Rre, -Rim], [Rim, Rre]]), np.concatenate([rl, 0 * rl]))
+        assert rel(A[e].cpu().numpy(), Ar) <= TOL
+        assert rel(rhs[e].cpu().numpy(), rr) <= TOL_RHS
+
+
+@pytest.mark.gpu
+def test_acoustics_errors():
+    from paper_1711_00984_b200.dpg import UltraweakAcousticsProblem, acoustics_ultraweak_element
+    from paper_1711_00984_b200 import preset_map
+
+    with pytest.raises(ValueError):
+        UltraweakAcousticsProblem(omega=0.0, alpha=1.0)
+    with pytest.raises(ValueError):
+        UltraweakAcousticsProblem(omega=1.0, alpha=1.0, load_pairing="bogus")
+    with pytest.raises(ValueError):
+        acoustics_ultraweak_element(UltraweakAcousticsProblem(1.0, 1.0), 0, 1, preset_map("identity"))
+    s = acoustics_ultraweak_element(UltraweakAcousticsProblem(1.0, 1.0), 1, 1, preset_map("identity"))
+    assert not s.l.any()
