@@ -425,7 +425,8 @@ def dpg_suite(device, fp64, hbm, reps=3):
             bb = trilinear_batch(E, 22, variable_coef=True)
             G, _ = gram_batched("H1", (5, 5, 5), bb.kind, bb.params, bb.coef)
         else:
-            G = adjoint_graph_gram_batched(pa, 2.0, 0.5, kind[:E], params[:E])
+            ba = trilinear_batch(E, 24)
+            G = adjoint_graph_gram_batched(pa, 2.0, 0.5, ba.kind, ba.params)
         B = torch.as_tensor(rng.standard_normal((E, m, n))).to(device)
         l = torch.as_tensor(rng.standard_normal((E, m))).to(device)
         t = timed(lambda: condense_batched(G, B, l, check=False))
@@ -435,6 +436,31 @@ def dpg_suite(device, fp64, hbm, reps=3):
                     "roofline_frac": E * F / t / 1e12 / fp64, "m": m, "n": n})
         del G, B, l
         torch.cuda.empty_cache()
+    # ultraweak acoustics stiffness B + load l (dpg.py:234-302), p0 = 3, p_r = 5, trilinear;
+    # FLOPs = 2 x the multiply-adds of the reference's 22 mixed_tens_term calls
+    # (_kernels.py:1908-1930: stage A L^3 n3 p0, stage B L^2 n2 p0 n3 p0, stage C L nt ny)
+    from paper_1711_00984_b200.dpg import acoustics_batched
+
+    p0, pq, E = 3, 5, 2048
+    L = pq + 1
+    bb = trilinear_batch(E, 23)
+    kind2 = torch.as_tensor(bb.kind).to(device)
+    params2 = torch.as_tensor(bb.params).to(device)
+    fg = torch.as_tensor(np.random.default_rng(9).uniform(0.5, 1.5, (E, L ** 3))).to(device)
+    t = timed(lambda: acoustics_batched(p0, pq, 1.5, kind2, params2, fg, block_form=True))
+    q = pq + 1
+    terms = [(0, 0, 0)] + [(0, 0, 0)] * 9 + [(a != 0, a != 1, a != 2) for a in range(3)] * 4
+    F = 0.0
+    for sh in terms:
+        n1, n2, n3 = (q - x for x in sh)
+        F += 2.0 * (L ** 3 * n3 * p0 + L * L * n2 * p0 * n3 * p0 + L * n1 * n2 * n3 * p0 ** 3)
+    m_, n_ = q ** 3 + 3 * pq * pq * q, 4 * p0 ** 3
+    byt = 8.0 * (2 * m_ * n_ + 4 * m_ * n_ + 2 * m_)  # Bre, Bim, B2, l
+    tf, tb = E * F / (fp64 * 1e12), E * byt / (hbm * 1e9)
+    out.append({"workload": f"dpg_acoustics_B_p0{p0}_pr{pq}_general", "elements_per_s": E / t,
+                "ms_per_step": t * 1e3, "bound": "fp64" if tf >= tb else "hbm",
+                "fp64_tflops_alg": E * F / t / 1e12, "hbm_write_gbs": E * byt / t / 1e9,
+                "roofline_frac": max(tf, tb) / t})
     return out
 
 
