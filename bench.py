@@ -447,7 +447,7 @@ def dpg_suite(device, fp64, hbm, reps=3):
     kind2 = torch.as_tensor(bb.kind).to(device)
     params2 = torch.as_tensor(bb.params).to(device)
     fg = torch.as_tensor(np.random.default_rng(9).uniform(0.5, 1.5, (E, L ** 3))).to(device)
-    t = timed(lambda: acoustics_batched(p0, pq, 1.5, kind2, params2, fg, block_form=True))
+    t = timed(lambda: acoustics_batched(p0, pq, 1.5, kind2, params2, fg, parts=False))
     q = pq + 1
     terms = [(0, 0, 0)] + [(0, 0, 0)] * 9 + [(a != 0, a != 1, a != 2) for a in range(3)] * 4
     F = 0.0
@@ -455,7 +455,7 @@ def dpg_suite(device, fp64, hbm, reps=3):
         n1, n2, n3 = (q - x for x in sh)
         F += 2.0 * (L ** 3 * n3 * p0 + L * L * n2 * p0 * n3 * p0 + L * n1 * n2 * n3 * p0 ** 3)
     m_, n_ = q ** 3 + 3 * pq * pq * q, 4 * p0 ** 3
-    byt = 8.0 * (2 * m_ * n_ + 4 * m_ * n_ + 2 * m_)  # Bre, Bim, B2, l
+    byt = 8.0 * (4 * m_ * n_ + 2 * m_)  # B2 (real block form) and l
     tf, tb = E * F / (fp64 * 1e12), E * byt / (hbm * 1e9)
     out.append({"workload": f"dpg_acoustics_B_p0{p0}_pr{pq}_general", "elements_per_s": E / t,
                 "ms_per_step": t * 1e3, "bound": "fp64" if tf >= tb else "hbm",

@@ -179,8 +179,9 @@ size_t hxg_acoustics_workspace_size(int p0, int pr, int L, int E);
  * velocity components, each p0^3 L2 functions, n = 4 p0^3 columns), test
  * order pr (H1 then H(div) rows, m = (pr+1)^3 + 3 pr^2 (pr+1)), L-point rule
  * (tables from hxg_make_tables(L)).
- *   Bre, Bim : [E][m][n] real / imaginary parts (row-major), required
+ *   Bre, Bim : [E][m][n] real / imaginary parts (row-major), or both NULL
  *   B2       : [E][2m][2n] real block form [[Bre, -Bim], [Bim, Bre]] or NULL
+ *              (at least one of the two forms)
  *   fgrid    : [E][L^3] source sampled at the tensor nodes (l, m, n), or NULL
  *   lre      : [E][2m] load in real block form [l_re; 0], or NULL
  *   pairing  : 0 velocity (the printed form), 1 pressure (dpg.py:83-90)

@@ -431,13 +431,16 @@ __device__ AcBlock ac_block(int b, int pr, double omega)
 }
 
 // One CTA per (block, element).  Per term: stage A (xi3) sA[l][m][i3][k3], stage B
-// (xi2) sBt[l][i2][k2][i3][k3], stage C (xi1) accumulated into the owner thread's
-// output entries (first term stores, later terms add).  Dynamic shared memory.
-__global__ void __launch_bounds__(256) acoustics_block_kernel(int p0, int pr, int L, double omega,
+// (xi2) sBt[l][i2][k2][i3][k3], stage C (xi1) accumulated into the block's entries in
+// shared memory (sOut).  The finished block is written once to each requested output:
+// its Bre or Bim part, zeros to the other part (the reference never writes those
+// blocks), and the four positions of the real block form B2 = [[Bre, -Bim], [Bim, Bre]].
+__global__ void __launch_bounds__(256) acoustics_block_kernel(int p0, int pr, int L, double omega, int c3,
                                                              const double *__restrict__ tab,
                                                              const double *__restrict__ F,
                                                              double *__restrict__ Bre,
-                                                             double *__restrict__ Bim)
+                                                             double *__restrict__ Bim,
+                                                             double *__restrict__ B2)
 {
     extern __shared__ double sm[];
     const int b = blockIdx.x, e = blockIdx.y;
@@ -447,13 +450,13 @@ __global__ void __launch_bounds__(256) acoustics_block_kernel(int p0, int pr, in
     const int L3 = L * L * L;
     const int sh0 = B.t[0].sh[0], sh1 = B.t[0].sh[1], sh2 = B.t[0].sh[2];  // shared by a block's terms
     const int n1 = q - sh0, n2 = q - sh1, n3 = q - sh2;
-    const int nt = n1 * n2 * n3;
-    // shared: 1D tables u[f][k][l] (f: chi, chi'), nu[k][l], w[l]; stage buffers
-    double *sU = sm;                       // [2][q + 1][L]
-    double *sNu = sU + 2 * (q + 1) * L;    // [p0][L]
-    double *sW = sNu + p0 * L;             // [L]
-    double *sA = sW + L;                   // [L][L][n3][p0]
-    double *sBt = sA + L * L * n3 * p0;    // [L][n2][p0][n3][p0]
+    // shared: 1D tables u[f][k][l] (f: chi, chi'), nu[k][l], w[l]; stage buffers for c3 digits i3
+    double *sU = sm;                         // [2][q + 1][L]
+    double *sNu = sU + 2 * (q + 1) * L;      // [p0][L]
+    double *sW = sNu + p0 * L;               // [L]
+    double *sA = sW + L;                     // [L][L][c3][p0]
+    double *sBt = sA + L * L * c3 * p0;      // [L][n2][p0][c3][p0]
+    double *sOut = sBt + L * n2 * p0 * c3 * p0;  // [n1 n2 c3][ny]
     for (int i = threadIdx.x; i < 2 * (q + 1) * L; i += blockDim.x) {
         const int f = i / ((q + 1) * L), r = i - f * (q + 1) * L, k = r / L, l = r - k * L;
         sU[i] = tab[TAB_T + (f * KT + k) * LT + l];
@@ -463,46 +466,68 @@ __global__ void __launch_bounds__(256) acoustics_block_kernel(int p0, int pr, in
         sNu[i] = tab[TAB_T + (1 * KT + k + 1) * LT + l];  // nu_k = chi'_{k+1}
     }
     for (int i = threadIdx.x; i < L; i += blockDim.x) sW[i] = tab[TAB_WTS + i];
-    double *out = (B.re ? Bre : Bim) + (long long)e * m * n;
     const double *Fe = F + (long long)e * AC_NF * L3;
-    for (int t = 0; t < B.nterm; ++t) {
-        const AcTerm T = B.t[t];
-        const double *g = Fe + (long long)T.field * L3;
-        const double *u1 = sU + (T.su[0] * (q + 1) + sh0) * L;
-        const double *u2 = sU + (T.su[1] * (q + 1) + sh1) * L;
-        const double *u3 = sU + (T.su[2] * (q + 1) + sh2) * L;
-        __syncthreads();  // tables ready / previous term's stage buffers consumed
-        // stage A: sum over n (xi3), _kernels.py:1908-1911
-        for (int i = threadIdx.x; i < L * L * n3 * p0; i += blockDim.x) {
-            const int lm = i / (n3 * p0), r = i - lm * (n3 * p0), i3 = r / p0, k3 = r - i3 * p0;
-            double s = 0.0;
-            for (int nn = 0; nn < L; ++nn)
-                s = fma(sW[nn] * g[lm * L + nn], u3[i3 * L + nn] * sNu[k3 * L + nn], s);
-            sA[i] = s;
+    // stages A and B are separable in the test digit i3: slabs of c3 digits, no recomputation
+    for (int i30 = 0; i30 < n3; i30 += c3) {
+        const int c = min(c3, n3 - i30);
+        const int nts = n1 * n2 * c;  // rows of this slab
+        for (int t = 0; t < B.nterm; ++t) {
+            const AcTerm T = B.t[t];
+            const double *g = Fe + (long long)T.field * L3;
+            const double *u1 = sU + (T.su[0] * (q + 1) + sh0) * L;
+            const double *u2 = sU + (T.su[1] * (q + 1) + sh1) * L;
+            const double *u3 = sU + (T.su[2] * (q + 1) + sh2 + i30) * L;
+            __syncthreads();  // tables ready / previous stage buffers consumed
+            // stage A: sum over n (xi3), _kernels.py:1908-1911
+            for (int i = threadIdx.x; i < L * L * c * p0; i += blockDim.x) {
+                const int lm = i / (c * p0), r = i - lm * (c * p0), i3 = r / p0, k3 = r - i3 * p0;
+                double s = 0.0;
+                for (int nn = 0; nn < L; ++nn)
+                    s = fma(sW[nn] * g[lm * L + nn], u3[i3 * L + nn] * sNu[k3 * L + nn], s);
+                sA[i] = s;
+            }
+            __syncthreads();
+            // stage B: sum over m (xi2), _kernels.py:1912-1918
+            const int nb2 = n2 * p0 * c * p0;
+            for (int i = threadIdx.x; i < L * nb2; i += blockDim.x) {
+                const int l = i / nb2, r = i - l * nb2;
+                const int i2 = r / (p0 * c * p0), r2 = r - i2 * (p0 * c * p0);
+                const int k2 = r2 / (c * p0), r3 = r2 - k2 * (c * p0);  // r3 = i3 * p0 + k3
+                double s = 0.0;
+                for (int mm = 0; mm < L; ++mm)
+                    s = fma(u2[i2 * L + mm] * sNu[k2 * L + mm] * sW[mm], sA[(l * L + mm) * c * p0 + r3], s);
+                sBt[i] = s;
+            }
+            __syncthreads();
+            // stage C: sum over l (xi1), _kernels.py:1919-1930; entry (i, k) of the slab
+            for (int idx = threadIdx.x; idx < nts * ny; idx += blockDim.x) {
+                const int i = idx / ny, k = idx - i * ny;
+                const int i1 = i % n1, i2 = (i / n1) % n2, i3 = i / (n1 * n2);
+                const int k1 = k % p0, k2 = (k / p0) % p0, k3 = k / (p0 * p0);
+                const int r = ((i2 * p0 + k2) * c + i3) * p0 + k3;
+                double s = 0.0;
+                for (int l = 0; l < L; ++l) s = fma(u1[i1 * L + l] * sNu[k1 * L + l] * sW[l], sBt[l * nb2 + r], s);
+                sOut[idx] = (t == 0 ? 0.0 : sOut[idx]) + T.scale * s;  // entry owned by this thread
+            }
         }
         __syncthreads();
-        // stage B: sum over m (xi2), _kernels.py:1912-1918
-        const int nb2 = n2 * p0 * n3 * p0;
-        for (int i = threadIdx.x; i < L * nb2; i += blockDim.x) {
-            const int l = i / nb2, r = i - l * nb2;
-            const int i2 = r / (p0 * n3 * p0), r2 = r - i2 * (p0 * n3 * p0);
-            const int k2 = r2 / (n3 * p0), r3 = r2 - k2 * (n3 * p0);  // r3 = i3 * p0 + k3
-            double s = 0.0;
-            for (int mm = 0; mm < L; ++mm)
-                s = fma(u2[i2 * L + mm] * sNu[k2 * L + mm] * sW[mm], sA[(l * L + mm) * n3 * p0 + r3], s);
-            sBt[i] = s;
-        }
-        __syncthreads();
-        // stage C: sum over l (xi1), _kernels.py:1919-1930; entry (i, k) of the block
-        for (int idx = threadIdx.x; idx < nt * ny; idx += blockDim.x) {
+        const int row0 = B.row_off + n1 * n2 * i30;
+        for (int idx = threadIdx.x; idx < nts * ny; idx += blockDim.x) {
             const int i = idx / ny, k = idx - i * ny;
-            const int i1 = i % n1, i2 = (i / n1) % n2, i3 = i / (n1 * n2);
-            const int k1 = k % p0, k2 = (k / p0) % p0, k3 = k / (p0 * p0);
-            const int r = ((i2 * p0 + k2) * n3 + i3) * p0 + k3;
-            double s = 0.0;
-            for (int l = 0; l < L; ++l) s = fma(u1[i1 * L + l] * sNu[k1 * L + l] * sW[l], sBt[l * nb2 + r], s);
-            double *o = out + (long long)(B.row_off + i) * n + B.col_blk * ny + k;
-            *o = (t == 0 ? 0.0 : *o) + T.scale * s;
+            const double v = sOut[idx];
+            const double re = B.re ? v : 0.0, im = B.re ? 0.0 : v;
+            const long long row = row0 + i, col = (long long)B.col_blk * ny + k;
+            if (Bre) {
+                Bre[((long long)e * m + row) * n + col] = re;
+                Bim[((long long)e * m + row) * n + col] = im;
+            }
+            if (B2) {
+                double *b2 = B2 + (long long)e * 4 * m * n;
+                __stcs(b2 + row * 2 * n + col, re);
+                __stcs(b2 + row * 2 * n + n + col, -im);
+                __stcs(b2 + (m + row) * 2 * n + col, im);
+                __stcs(b2 + (m + row) * 2 * n + n + col, re);
+            }
         }
     }
 }
@@ -553,29 +578,11 @@ __global__ void acoustics_load_kernel(int pr, int L, int E, int pairing, const d
     }
 }
 
-// real block form [[Bre, -Bim], [Bim, Bre]] (dpg.py:322-323)
-__global__ void block_form_kernel(int m, int n, int E, const double *__restrict__ Bre,
-                                  const double *__restrict__ Bim, double *__restrict__ B2)
-{
-    const long long per = 4LL * m * n;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)E * per;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long e = idx / per, rc = idx - e * per;
-        const int r = (int)(rc / (2 * n)), c = (int)(rc - (long long)r * 2 * n);
-        const int R = r < m ? r : r - m, C = c < n ? c : c - n;
-        const long long src = (e * m + R) * n + C;
-        double v;
-        if ((r < m) == (c < n)) v = Bre[src];
-        else v = r < m ? -Bim[src] : Bim[src];
-        B2[idx] = v;
-    }
-}
-
-size_t ac_smem_bytes(int p0, int pr, int L)
+size_t ac_smem_bytes(int p0, int pr, int L, int c3)
 {
     const int q = pr + 1;
-    return sizeof(double) * ((size_t)2 * (q + 1) * L + (size_t)p0 * L + L + (size_t)L * L * q * p0 +
-                             (size_t)L * q * p0 * q * p0);
+    return sizeof(double) * ((size_t)2 * (q + 1) * L + (size_t)p0 * L + L + (size_t)L * L * c3 * p0 +
+                             (size_t)L * q * p0 * c3 * p0 + (size_t)q * q * c3 * p0 * p0 * p0);
 }
 
 int grid_for(long long work, int threads)
@@ -658,26 +665,22 @@ int hxg_acoustics_batched(int p0, int pr, double omega, int L, int E, const int 
     if (p0 < 1 || pr < p0 || pr + 2 > KT || L < 1 || L > LT) return HXG_ERR_ORDER;
     if (E < 0 || pairing < 0 || pairing > 1) return HXG_ERR_ARG;
     if (E == 0) return HXG_OK;
-    if (!kind || !params || !tables || !Bre || !Bim || (lre && !fgrid)) return HXG_ERR_ARG;
+    if (!kind || !params || !tables || (!Bre != !Bim) || (!Bre && !B2) || (lre && !fgrid)) return HXG_ERR_ARG;
     if (!workspace || ws_bytes < hxg_acoustics_workspace_size(p0, pr, L, E)) return HXG_ERR_WORKSPACE;
-    const size_t smem = ac_smem_bytes(p0, pr, L);
+    int c3 = pr + 1;  // i3 slab: the largest that fits the shared-memory budget
+    while (c3 > 1 && ac_smem_bytes(p0, pr, L, c3) > 200 * 1024) --c3;
+    const size_t smem = ac_smem_bytes(p0, pr, L, c3);
     if (smem > 227 * 1024) return HXG_ERR_ORDER;
+    const int m = (pr + 1) * (pr + 1) * (pr + 1) + 3 * (pr + 1) * pr * pr;
     cudaStream_t st = (cudaStream_t)stream;
     double *F = (double *)workspace;
     if (status && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
     acoustics_geom_kernel<<<grid_for((long long)E * L * L * L, 256), 256, 0, st>>>(L, E, kind, params, tables,
                                                                                   F, status);
-    const int q = pr + 1, m = q * q * q + 3 * q * pr * pr, n = 4 * p0 * p0 * p0;
-    // blocks no term writes (Bre[:mw, :ny], Bim[:mw, ny:], ...) are zero
-    if (cudaMemsetAsync(Bre, 0, sizeof(double) * (size_t)E * m * n, st) != cudaSuccess ||
-        cudaMemsetAsync(Bim, 0, sizeof(double) * (size_t)E * m * n, st) != cudaSuccess)
-        return HXG_ERR_CUDA;
     if (cudaFuncSetAttribute(acoustics_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return HXG_ERR_CUDA;
-    acoustics_block_kernel<<<dim3(16, E), 256, smem, st>>>(p0, pr, L, omega, tables, F, Bre, Bim);
-    if (B2)
-        block_form_kernel<<<grid_for(4LL * E * m * n, 256), 256, 0, st>>>(m, n, E, Bre, Bim, B2);
+    acoustics_block_kernel<<<dim3(16, E), 256, smem, st>>>(p0, pr, L, omega, c3, tables, F, Bre, Bim, B2);
     if (lre)
         acoustics_load_kernel<<<grid_for((long long)E * m, 128), 128, 0, st>>>(pr, L, E, pairing, tables, F,
                                                                              fgrid, lre);

@@ -259,12 +259,16 @@ class UltraweakAcousticsProblem:
 
 
 def acoustics_batched(p0: int, pr: int, omega: float, kind, params, fgrid=None, *,
-                      pairing: str = "velocity", block_form: bool = True, device=None, stream=None):
+                      pairing: str = "velocity", block_form: bool = True, parts: bool = True,
+                      device=None, stream=None):
     """Batched ultraweak-acoustics stiffness (dpg.py:234-277) and load
     (dpg.py:280-302) on the device, rule L = pr + 1.  kind int32 [E], params
     float64 [E, 24]; fgrid float64 [E, L^3] (source at the tensor nodes, point
     (l, m, n) -> (l L + m) L + n) or None.  Returns (Bre [E, m, n],
-    Bim [E, m, n], B2 [E, 2m, 2n] or None, l [E, 2m] or None, status)."""
+    Bim [E, m, n] (None unless ``parts``), B2 [E, 2m, 2n] (None unless
+    ``block_form``), l [E, 2m] or None, status)."""
+    if not (parts or block_form):
+        raise ValueError("request at least one of parts / block_form")
     from .engine import _check
 
     eng = _engine(device)
@@ -277,8 +281,8 @@ def acoustics_batched(p0: int, pr: int, omega: float, kind, params, fgrid=None, 
     q = pr + 1
     m = q ** 3 + 3 * pr * pr * q
     n = 4 * p0 ** 3
-    Bre = torch.empty((E, m, n), dtype=torch.float64, device=dev)
-    Bim = torch.empty((E, m, n), dtype=torch.float64, device=dev)
+    Bre = torch.empty((E, m, n), dtype=torch.float64, device=dev) if parts else None
+    Bim = torch.empty((E, m, n), dtype=torch.float64, device=dev) if parts else None
     B2 = torch.empty((E, 2 * m, 2 * n), dtype=torch.float64, device=dev) if block_form else None
     lre = None
     if fgrid is not None:
@@ -321,7 +325,7 @@ def acoustics_ultraweak_element(problem: UltraweakAcousticsProblem, p0: int, dp:
     fg = _source_grid(problem.f, emap, L)
     _, _, B2, lre, status = acoustics_batched(
         p0, pr, problem.omega, np.array([emap.kind_code], np.int32), emap.params.reshape(1, 24),
-        None if fg is None else fg[None], pairing=problem.load_pairing)
+        None if fg is None else fg[None], pairing=problem.load_pairing, parts=False)
     B = B2[0].cpu().numpy()
     m = B.shape[0] // 2
     l = lre[0].cpu().numpy() if lre is not None else np.zeros(2 * m)
