@@ -165,7 +165,7 @@ __device__ __forceinline__ void cd_dmma(double &d0, double &d1, double a, double
                  : "d"(a), "d"(b));
 }
 
-constexpr int CD_PS = CD_TT + 8;  // panel row stride (doubles): k rows t, t+1 fall in opposite bank halves
+constexpr int CD_PS = CD_NB + 4;  // panel row stride (doubles): 8-byte fragment loads hit 16 distinct banks
 
 // One CTA (8 warps) per element.  Per panel of CD_NB columns:
 //   (a) warp 0 factors the diagonal block L_D (unblocked, shared memory) and forms
@@ -179,13 +179,13 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
 {
     const int Mt = m + n + 1;
     double *__restrict__ W = Wall + (long long)blockIdx.x * Mt * Mt;
-    // sPi: panel rows of tile ti, [t][row]; sPj: of tile tj; sD (L_D, lower) lives in the
+    // sPi: panel rows of tile ti, [row][t]; sPj: of tile tj; sD (L_D, lower) lives in the
     // sPj space while the diagonal block is factored; sDi = L_D^-1, zero padded to CD_NB
-    __shared__ __align__(16) double s_raw[2 * CD_NB * CD_PS + CD_NB * (CD_NB + 1)];
+    __shared__ __align__(16) double s_raw[2 * CD_TT * CD_PS + CD_NB * CD_PS];
     double(*sPi)[CD_PS] = reinterpret_cast<double(*)[CD_PS]>(s_raw);
-    double(*sPj)[CD_PS] = reinterpret_cast<double(*)[CD_PS]>(s_raw + CD_NB * CD_PS);
-    double(*sD)[CD_NB + 1] = reinterpret_cast<double(*)[CD_NB + 1]>(s_raw + CD_NB * CD_PS);
-    double(*sDi)[CD_NB + 1] = reinterpret_cast<double(*)[CD_NB + 1]>(s_raw + 2 * CD_NB * CD_PS);
+    double(*sPj)[CD_PS] = reinterpret_cast<double(*)[CD_PS]>(s_raw + CD_TT * CD_PS);
+    double(*sD)[CD_PS] = reinterpret_cast<double(*)[CD_PS]>(s_raw + CD_TT * CD_PS);
+    double(*sDi)[CD_PS] = reinterpret_cast<double(*)[CD_PS]>(s_raw + 2 * CD_TT * CD_PS);
     __shared__ int s_bad;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g8 = lane >> 2, t4 = lane & 3;
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
             const int ib = r0 + ti * CD_TT;
             for (int idx = tid; idx < CD_TT * CD_NB; idx += CD_THREADS) {
                 const int rr = idx / CD_NB, t = idx - rr * CD_NB;
-                sPi[t][rr] = (t < kb && ib + rr < Mt) ? W[(long long)(ib + rr) * Mt + k0 + t] : 0.0;
+                sPi[rr][t] = (t < kb && ib + rr < Mt) ? W[(long long)(ib + rr) * Mt + k0 + t] : 0.0;
             }
             __syncthreads();
             // (b) X = P L_D^-T: warp w owns rows 8w..8w+7 of the tile (in place)
@@ -253,21 +253,21 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
 #pragma unroll
                 for (int ks = 0; ks < CD_NB / 4; ++ks) {
                     const int t = 4 * ks + t4;
-                    const double a = sPi[t][8 * warp + g8];
+                    const double a = sPi[8 * warp + g8][t];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) cd_dmma(acc[q][0], acc[q][1], a, sDi[8 * q + g8][t]);
                 }
                 __syncwarp();
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    sPi[8 * q + 2 * t4][8 * warp + g8] = acc[q][0];
-                    sPi[8 * q + 2 * t4 + 1][8 * warp + g8] = acc[q][1];
+                    sPi[8 * warp + g8][8 * q + 2 * t4] = acc[q][0];
+                    sPi[8 * warp + g8][8 * q + 2 * t4 + 1] = acc[q][1];
                 }
             }
             __syncthreads();
             for (int idx = tid; idx < CD_TT * CD_NB; idx += CD_THREADS) {
                 const int rr = idx / CD_NB, t = idx - rr * CD_NB;
-                if (t < kb && ib + rr < Mt) W[(long long)(ib + rr) * Mt + k0 + t] = sPi[t][rr];
+                if (t < kb && ib + rr < Mt) W[(long long)(ib + rr) * Mt + k0 + t] = sPi[rr][t];
             }
             // (c) trailing update, warp w: rows 16 (w >> 1) .. +16, columns 32 (w & 1) .. +32
             const int rb = warp >> 1, cb = warp & 1;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                 if (tj < ti) {
                     for (int idx = tid; idx < CD_TT * CD_NB; idx += CD_THREADS) {
                         const int rr = idx / CD_NB, t = idx - rr * CD_NB;
-                        sPj[t][rr] = (t < kb && jb + rr < Mt) ? W[(long long)(jb + rr) * Mt + k0 + t] : 0.0;
+                        sPj[rr][t] = (t < kb && jb + rr < Mt) ? W[(long long)(jb + rr) * Mt + k0 + t] : 0.0;
                     }
                 }
                 __syncthreads();
@@ -294,9 +294,9 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                         const int t = 4 * ks + t4;
                         double av[2], bv[4];
 #pragma unroll
-                        for (int a = 0; a < 2; ++a) av[a] = sPi[t][16 * rb + 8 * a + g8];
+                        for (int a = 0; a < 2; ++a) av[a] = sPi[16 * rb + 8 * a + g8][t];
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) bv[b] = Pj[t][32 * cb + 8 * b + g8];
+                        for (int b = 0; b < 4; ++b) bv[b] = Pj[32 * cb + 8 * b + g8][t];
 #pragma unroll
                         for (int a = 0; a < 2; ++a)
 #pragma unroll

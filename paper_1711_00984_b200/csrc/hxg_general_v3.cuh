@@ -51,14 +51,26 @@ struct V3Cfg {
         return m;
     }
     static constexpr int NT = maxt();
+    // test digits i3 per work unit: the packed row segment of a unit is K * C12 long, so
+    // each bulk copy moves K times as many bytes (the TMA engine accepts about one small
+    // copy per ~32 SM cycles: measured ~3.4 TB/s for ~400-byte rows); HBM-bound spaces
+    // use K = 2 with one staging buffer, FP64-bound spaces K = 1 with two
+#ifndef HXG_V3_K_HDIV
+#define HXG_V3_K_HDIV 2  // measured best of 1..4 for H(div) p7 (profiles/v3_k_r01.txt)
+#endif
+#ifndef HXG_V3_K_L2
+#define HXG_V3_K_L2 4  // measured best of 1..4 for L2 p7
+#endif
+    static constexpr int K = P <= 2 ? 1 : (S == HDIV ? HXG_V3_K_HDIV : (S == L2 ? HXG_V3_K_L2 : 1));
+    static constexpr int NSTG = K == 1 ? 2 : 1;  // staging buffers per warp
     static constexpr int LP = (L + 1) & ~1;      // sT row stride
-    static constexpr int SW = ((C12 + 1 + 1) / 2) * 2;  // staging row stride (even, >= C12 + 1)
+    static constexpr int SW = ((K * C12 + 1 + 1) / 2) * 2;  // staging row stride (even, >= K C12 + 1)
     // per-warp shared memory (doubles)
     static constexpr int W_P = 0;                       // [NT][8]   stage-A 1D products
-    static constexpr int W_A = W_P + NT * 8;            // [NG][8][8] Abar (rows m, cols l; zero padded)
-    static constexpr int W_B = W_A + NG * 64;           // [NH][8][8] B_h (rows i2, cols l)
-    static constexpr int W_S = W_B + NH * 64;           // [2][8][SW] staging
-    static constexpr int W_TOT = W_S + 2 * C2::N1 * SW;  // [2][N1][SW] staging
+    static constexpr int W_A = W_P + NT * 8;            // [K][NG][8][8] Abar (rows m, cols l; zero padded)
+    static constexpr int W_B = W_A + K * NG * 64;       // [NH][8][8] B_h (rows i2, cols l)
+    static constexpr int W_S = W_B + NH * 64;           // [NSTG][N1][SW] staging
+    static constexpr int W_TOT = W_S + NSTG * C2::N1 * SW;
     static constexpr int OFF_T = 0;                     // CTA-shared [2][KT][LP]
     static constexpr int OFF_W = 2 * KT * LP;
     // p <= 3: the element's metric fields are evaluated in the kernel into shared
@@ -66,9 +78,12 @@ struct V3Cfg {
     static constexpr bool FUSED = P <= 3;
     static constexpr int OFF_M = OFF_W + V3_WARPS * W_TOT;
     static constexpr int SMEM_BYTES = (OFF_M + (FUSED ? NF * L3 : 0)) * 8 + 16;
+    __host__ __device__ static constexpr int kcnt(int r) { return (r + K - 1) / K; }  // units over r digits i3
     __host__ __device__ static constexpr int pair_units(int a, int b)
     {
-        return a == b ? n(a, 2) * (n(a, 2) + 1) / 2 : n(a, 2) * n(b, 2);
+        int u = 0;
+        for (int j3 = 0; j3 < n(b, 2); ++j3) u += kcnt(a == b ? n(a, 2) - j3 : n(a, 2));
+        return u;
     }
     __host__ __device__ static constexpr int units()
     {
@@ -151,14 +166,22 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
     const int lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
     double *sP = W + C::W_P, *sA = W + C::W_A, *sBw = W + C::W_B;
 
-    // ---------------- stage A: contract xi3 ----------------
+    constexpr int K = C::K;
+    constexpr int n3a = C::n(A, 2);
+    const int kc = cmin(K, n3a - i3);  // test digits i3 .. i3 + kc - 1 in this unit
+    // ---------------- stage A: contract xi3 (per test digit of the unit) ----------------
+    for (int kk = 0; kk < K; ++kk) {
+    if (kk >= kc) break;
+    const int i3k = i3 + kk;
+    double *sAk = sA + kk * C::NG * 64;
+    __syncwarp();
     for (int o = lane; o < pp.nt * 8; o += 32) {
         const int t = o >> 3, n = o & 7;
         int fr = 0, fs = 0;
 #pragma unroll
         for (int tt = 0; tt < pp.nt; ++tt)
             if (tt == t) { fr = pp.t_fr[tt]; fs = pp.t_fs[tt]; }
-        sP[o] = n < L ? sT[(fr * KT + i3 + sha2) * LP + n] * sT[(fs * KT + j3 + shb2) * LP + n] : 0.0;
+        sP[o] = n < L ? sT[(fr * KT + i3k + sha2) * LP + n] * sT[(fs * KT + j3 + shb2) * LP + n] : 0.0;
     }
     __syncwarp();
     constexpr int NPASS = (L * L + 31) / 32;  // metric points per lane
@@ -195,10 +218,11 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
             const int lm = lane + 32 * q;
             if (lm < L * L) {
                 const int l = lm / L, m = lm - l * L;
-                sA[(g * 8 + m) * 8 + l] = acc[q];
+                sAk[(g * 8 + m) * 8 + l] = acc[q];
             }
         }
     }
+    }  // kk
     __syncwarp();
 
     // ---------------- per-unit operand registers ----------------
@@ -268,6 +292,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
     }
 
     const int I0 = offA + ncols * i3;
+    const int ncu = kc * ncols;  // columns of this unit's row segments
     for (int j2 = 0; j2 < n2b; ++j2) {
         // ---------------- stage B: contract xi2 on DMMA ----------------
         double Tb[2][LQ];
@@ -278,6 +303,14 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
                 const int m = ks * 4 + t4;
                 Tb[fs][ks] = m < L ? sT[(fs * KT + j2 + shb1) * LP + m] : 0.0;
             }
+        const int J = offB + g8 + n1b * (j2 + n2b * j3);  // row of this lane's j1 = g8
+        const int goff = J * N - J * (J - 1) / 2 - J + I0;
+        const int pad = (epar + goff) & 1;
+        double *sS = W + C::W_S + (C::NSTG == 2 ? buf : 0) * C::C2::N1 * SW;
+        for (int kk = 0; kk < K; ++kk) {
+        if (kk >= kc) break;
+        const double *sAk = sA + kk * C::NG * 64;
+        if (kk > 0) __syncwarp();  // previous digit's stage C has read B_h
         // two h chains at a time: independent DMMA accumulators hide the DMMA latency
 #pragma unroll
         for (int h0 = 0; h0 < pp.nh; h0 += 2) {
@@ -289,7 +322,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
                     const int g = (h0 + c < MAXH) ? GL.g[h0 + c][q / LQ] : -1, ks = q % LQ;
                     if (h0 + c < pp.nh && g >= 0) {
                         const double av = Ta[pp.g_fr[g]][ks] * Tb[pp.g_fs[g]][ks];
-                        const double bv = sA[(g * 8 + ks * 4 + t4) * 8 + g8];
+                        const double bv = sAk[(g * 8 + ks * 4 + t4) * 8 + g8];
                         dmma_8x8x4_keep(d[c][0], d[c][1], av, bv, keep);
                     }
                 }
@@ -302,15 +335,14 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
                 }
         }
         __syncwarp();
-        // staging buffer `buf` was last read by the bulk copies issued two rows-groups ago
-        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-        __syncwarp();
-
-        double *sS = W + C::W_S + buf * C::C2::N1 * SW;
-        const int J = offB + g8 + n1b * (j2 + n2b * j3);  // row of this lane's j1 = g8
-        const int goff = J * N - J * (J - 1) / 2 - J + I0;
-        const int pad = (epar + goff) & 1;
-        double *srow = sS + g8 * SW + pad;
+        if (kk == 0) {
+            // staging buffer `buf` was last read by the bulk copies issued two row groups ago
+            // (NSTG == 2) or by the previous row group's copies (NSTG == 1)
+            if constexpr (C::NSTG == 2) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            __syncwarp();
+        }
+        double *srow = sS + g8 * SW + pad + kk * ncols;
         // ---------------- stage C: contract xi1 on DMMA ----------------
         if constexpr (YF) {
 #pragma unroll
@@ -360,6 +392,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
                     }
             }
         }
+        }  // kk
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
         // ---------------- write-out: lane j1 copies packed row J from column max(J, I0) ----------------
@@ -370,17 +403,17 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
             const int padr = (epar + goffr) & 1;
             const int csr = Jr > I0 ? Jr - I0 : 0;
             const double *srcr = sS + j1 * SW + padr;
-            for (int c = csr + lane; c < ncols; c += 32) outE[goffr + c] = srcr[c];
+            for (int c = csr + lane; c < ncu; c += 32) outE[goffr + c] = srcr[c];
         }
         if (false) {
 #else
         if (g8 < n1b && t4 == 0) {
 #endif
             const int cs = J > I0 ? J - I0 : 0;
-            if (cs < ncols) {
-                const double *src = srow + cs;
+            if (cs < ncu) {
+                const double *src = sS + g8 * SW + pad + cs;
                 double *dst = outE + goff + cs;
-                int len = ncols - cs;
+                int len = ncu - cs;
                 if (reinterpret_cast<size_t>(dst) & 8) {
                     __stcs(dst, *src);
                     ++dst;
@@ -397,7 +430,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
             }
         }
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-        buf ^= 1;
+        if constexpr (C::NSTG == 2) buf ^= 1;
         __syncwarp();  // reconverge after the divergent write-out: the next mma.sync needs the full warp
     }
 #ifdef HXG_V3_DEBUG2
@@ -589,15 +622,15 @@ __global__ void __launch_bounds__(V3_THREADS, (V3Cfg<S, P, L>::MINB))
                     const int cnt = C::pair_units(a, b);
                     if (rem < cnt) {
                         pair = a * 3 + b;
-                        if (a == b) {  // j3 <= i3 < n3
-                            const int n3 = C::n(a, 2);
+                        const int n3 = C::n(a, 2);
+                        if (a == b) {  // j3 <= i3 < n3, i3 = j3 + K r
                             int jj = 0, r = rem;
-                            while (r >= n3 - jj) { r -= n3 - jj; ++jj; }
+                            while (r >= C::kcnt(n3 - jj)) { r -= C::kcnt(n3 - jj); ++jj; }
                             j3 = jj;
-                            i3 = jj + r;
+                            i3 = jj + C::K * r;
                         } else {
-                            j3 = rem / C::n(a, 2);
-                            i3 = rem - j3 * C::n(a, 2);
+                            j3 = rem / C::kcnt(n3);
+                            i3 = C::K * (rem - j3 * C::kcnt(n3));
                         }
                     } else {
                         rem -= cnt;

@@ -54,11 +54,19 @@ struct V4Cfg {
     static constexpr int OFF_T = 0;
     static constexpr int OFF_W = 2 * KT * LP;
     static constexpr int SMEM_BYTES = (OFF_W + WARPS * W_TOT) * 8 + 16;
-    static constexpr int NU = V3Cfg<S, P, L>::NU;
+    // one (j3, i3) digit pair per work unit (v3 may group several i3 per unit)
     __host__ __device__ static constexpr int pair_units(int a, int b)
     {
-        return V3Cfg<S, P, L>::pair_units(a, b);
+        return a == b ? n(a, 2) * (n(a, 2) + 1) / 2 : n(a, 2) * n(b, 2);
     }
+    __host__ __device__ static constexpr int units()
+    {
+        int u = 0;
+        for (int b = 0; b < NB; ++b)
+            for (int a = b; a < NB; ++a) u += pair_units(a, b);
+        return u;
+    }
+    static constexpr int NU = units();
     static constexpr int MINB = cmin(4, (228 * 1024) / (SMEM_BYTES + 1024));
     // stage-C factorization per block pair, FP64-pipe cost with tiles (x8):
     // B-form per 8 test digits i2: n1a x MB x NKS DMMA (+ a DMUL per lane);
