@@ -55,13 +55,17 @@ struct V3Cfg {
     // each bulk copy moves K times as many bytes (the TMA engine accepts about one small
     // copy per ~32 SM cycles: measured ~3.4 TB/s for ~400-byte rows); HBM-bound spaces
     // use K = 2 with one staging buffer, FP64-bound spaces K = 1 with two
-#ifndef HXG_V3_K_HDIV
-#define HXG_V3_K_HDIV 2  // measured best of 1..4 for H(div) p7 (profiles/v3_k_r01.txt)
+    // measured best of K = 1..4 (profiles/v3_k_r01.txt): H(div) 4 at p <= 4 and p = 7,
+    // 2 at p = 5, 6; L2 (p = 7) 4
+#ifdef HXG_V3_K_HDIV
+    static constexpr int KHD = HXG_V3_K_HDIV;
+#else
+    static constexpr int KHD = (P == 5 || P == 6) ? 2 : 4;
 #endif
 #ifndef HXG_V3_K_L2
-#define HXG_V3_K_L2 4  // measured best of 1..4 for L2 p7
+#define HXG_V3_K_L2 4
 #endif
-    static constexpr int K = P <= 2 ? 1 : (S == HDIV ? HXG_V3_K_HDIV : (S == L2 ? HXG_V3_K_L2 : 1));
+    static constexpr int K = P <= 2 ? 1 : (S == HDIV ? KHD : (S == L2 ? HXG_V3_K_L2 : 1));
     static constexpr int NSTG = K == 1 ? 2 : 1;  // staging buffers per warp
     static constexpr int LP = (L + 1) & ~1;      // sT row stride
     static constexpr int SW = ((K * C12 + 1 + 1) / 2) * 2;  // staging row stride (even, >= K C12 + 1)
