@@ -499,15 +499,38 @@ __global__ void __launch_bounds__(256) acoustics_block_kernel(int p0, int pr, in
                 sBt[i] = s;
             }
             __syncthreads();
-            // stage C: sum over l (xi1), _kernels.py:1919-1930; entry (i, k) of the slab
-            for (int idx = threadIdx.x; idx < nts * ny; idx += blockDim.x) {
-                const int i = idx / ny, k = idx - i * ny;
-                const int i1 = i % n1, i2 = (i / n1) % n2, i3 = i / (n1 * n2);
-                const int k1 = k % p0, k2 = (k / p0) % p0, k3 = k / (p0 * p0);
-                const int r = ((i2 * p0 + k2) * c + i3) * p0 + k3;
-                double s = 0.0;
-                for (int l = 0; l < L; ++l) s = fma(u1[i1 * L + l] * sNu[k1 * L + l] * sW[l], sBt[l * nb2 + r], s);
-                sOut[idx] = (t == 0 ? 0.0 : sOut[idx]) + T.scale * s;  // entry owned by this thread
+            // stage C: sum over l (xi1), _kernels.py:1919-1930.  A thread owns trial column
+            // k (and k + kt, ...) for the rows i = rg, rg + nrg, ... of the slab: the trial
+            // factors nu_k1(l) w_l sit in registers, the row digits advance incrementally
+            {
+                const int kt = ny < (int)blockDim.x ? ny : (int)blockDim.x;
+                const int nrg = blockDim.x / kt;
+                const int rg = threadIdx.x / kt, kl = threadIdx.x - rg * kt;
+                if (rg < nrg) {
+                    for (int k = kl; k < ny; k += kt) {
+                        const int k1 = k % p0, k2 = (k / p0) % p0, k3 = k / (p0 * p0);
+                        double nuw[LT];
+#pragma unroll
+                        for (int l = 0; l < LT; ++l) nuw[l] = l < L ? sNu[k1 * L + l] * sW[l] : 0.0;
+                        const int rk = k2 * c * p0 + k3;  // r = i2 (p0 c p0) + k2 (c p0) + i3 p0 + k3
+                        int i1 = rg % n1, i2 = (rg / n1) % n2, i3 = rg / (n1 * n2);
+                        for (int i = rg; i < nts; i += nrg) {
+                            const double *u = u1 + i1 * L;
+                            const double *bt = sBt + i2 * (p0 * c * p0) + rk + i3 * p0;
+                            double s = 0.0;
+#pragma unroll
+                            for (int l = 0; l < LT; ++l)
+                                if (l < L) s = fma(u[l] * nuw[l], bt[l * nb2], s);
+                            double &o = sOut[i * ny + k];  // entry owned by this thread
+                            o = (t == 0 ? 0.0 : o) + T.scale * s;
+                            i1 += nrg;
+                            while (i1 >= n1) {
+                                i1 -= n1;
+                                if (++i2 == n2) { i2 = 0; ++i3; }
+                            }
+                        }
+                    }
+                }
             }
         }
         __syncthreads();

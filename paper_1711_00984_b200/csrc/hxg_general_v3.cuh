@@ -55,12 +55,12 @@ struct V3Cfg {
     // each bulk copy moves K times as many bytes (the TMA engine accepts about one small
     // copy per ~32 SM cycles: measured ~3.4 TB/s for ~400-byte rows); HBM-bound spaces
     // use K = 2 with one staging buffer, FP64-bound spaces K = 1 with two
-    // measured best of K = 1..4 (profiles/v3_k_r01.txt): H(div) 4 at p <= 4 and p = 7,
-    // 2 at p = 5, 6; L2 (p = 7) 4
+    // measured best of K = 1..4 (profiles/v3_k_r01.txt, sweep_r01.json): H(div) 4 at
+    // p <= 4 and p = 7, 2 at p = 6, 1 at p = 5; L2 (p = 7) 4
 #ifdef HXG_V3_K_HDIV
     static constexpr int KHD = HXG_V3_K_HDIV;
 #else
-    static constexpr int KHD = (P == 5 || P == 6) ? 2 : 4;
+    static constexpr int KHD = P == 5 ? 1 : (P == 6 ? 2 : 4);
 #endif
 #ifndef HXG_V3_K_L2
 #define HXG_V3_K_L2 4
