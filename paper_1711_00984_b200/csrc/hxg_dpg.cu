@@ -81,47 +81,61 @@ __global__ void graph_mixed_kernel(int pr, double omega, const double *__restric
 // from the packed H1 Gram gq [E][mw(mw+1)/2], the packed H(div) Gram
 // gv [E][mv(mv+1)/2] and S [mw][mv] (NULL: include_mixed=False).  Writes the
 // full matrices [E][2m][2m] and/or their packed upper triangles.
-__device__ __forceinline__ double graph_entry(long long e, int r, int c, int mw, int mv,
-                                              const double *__restrict__ gq,
-                                              const double *__restrict__ gv,
-                                              const double *__restrict__ S)
+// one warp per output row (e, r) of the real block form: per row the source rows are
+// fixed, so each output segment is a contiguous copy (packed Gram row, S row) or a
+// strided gather (S column, the mirrored lower part of the full layout)
+__device__ __forceinline__ void graph_row_segment(double *__restrict__ dst, int c0, int c1, int r,
+                                                  int mw, int mv, const double *__restrict__ gqe,
+                                                  const double *__restrict__ gve,
+                                                  const double *__restrict__ S, int lane)
 {
+    // dst[c] for c in [c0, c1) of row r; every [c0, c1) here lies inside one quadrant
     const int m = mw + mv;
-    const bool br = r >= m, bc = c >= m;
-    const int R = br ? r - m : r, C = bc ? c - m : c;
-    if (br == bc) {
-        if (R < mw && C < mw) return gq[e * ((long long)mw * (mw + 1) / 2) + packed_index(R, C, mw)];
-        if (R >= mw && C >= mw)
-            return gv[e * ((long long)mv * (mv + 1) / 2) + packed_index(R - mw, C - mw, mv)];
-        return 0.0;
+    const bool br = r >= m;
+    const int R = br ? r - m : r;
+    for (int c = c0 + lane; c < c1; c += 32) {
+        const bool bc = c >= m;
+        const int C = bc ? c - m : c;
+        double v = 0.0;
+        if (br == bc) {
+            if (R < mw && C < mw) {
+                const int lo = min(R, C), hi = max(R, C);
+                v = gqe[lo * mw - lo * (lo - 1) / 2 + (hi - lo)];
+            } else if (R >= mw && C >= mw) {
+                const int lo = min(R, C) - mw, hi = max(R, C) - mw;
+                v = gve[lo * mv - lo * (lo - 1) / 2 + (hi - lo)];
+            }
+        } else if (S) {
+            double im = 0.0;
+            if (R < mw && C >= mw) im = S[R * mv + (C - mw)];
+            else if (R >= mw && C < mw) im = -S[C * mv + (R - mw)];
+            v = br ? im : -im;
+        }
+        dst[c] = v;
     }
-    if (!S) return 0.0;
-    double im = 0.0;
-    if (R < mw && C >= mw) im = S[(long long)R * mv + (C - mw)];
-    else if (R >= mw && C < mw) im = -S[(long long)C * mv + (R - mw)];
-    return br ? im : -im;
 }
 
-// one warp per output row (e, r): coalesced stores, contiguous packed-row reads
 __global__ void graph_assemble_kernel(int mw, int mv, int E, const double *__restrict__ gq,
                                       const double *__restrict__ gv, const double *__restrict__ S,
                                       double *__restrict__ full, double *__restrict__ packed)
 {
     const int M2 = 2 * (mw + mv);
     const long long NN = (long long)M2 * M2, P = (long long)M2 * (M2 + 1) / 2;
+    const long long Pq = (long long)mw * (mw + 1) / 2, Pv = (long long)mv * (mv + 1) / 2;
     const int lane = threadIdx.x & 31;
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
          row < (long long)E * M2; row += nw) {
         const long long e = row / M2;
         const int r = (int)(row - e * M2);
+        const double *gqe = gq + e * Pq, *gve = gv + e * Pv;
         if (full) {
             double *dst = full + e * NN + (long long)r * M2;
-            for (int c = lane; c < M2; c += 32) dst[c] = graph_entry(e, r, c, mw, mv, gq, gv, S);
+            graph_row_segment(dst, 0, M2, r, mw, mv, gqe, gve, S, lane);
         }
         if (packed) {
             double *dst = packed + e * P + (long long)r * M2 - (long long)r * (r - 1) / 2 - r;
-            for (int c = r + lane; c < M2; c += 32) dst[c] = graph_entry(e, r, c, mw, mv, gq, gv, S);
+            graph_row_segment(dst, r, M2, r, mw, mv, gqe, gve, S, lane);
         }
     }
 }
