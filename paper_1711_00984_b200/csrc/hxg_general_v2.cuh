@@ -206,6 +206,14 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef HXG_V2_PF_MINNH
 #define HXG_V2_PF_MINNH 3
 #endif
+// B-form: trial rows j1 beyond the last full 8-row tile on DFMA instead of a
+// mostly-empty DMMA row tile (both share the FP64 pipe), for at most HXG_V2_DREM
+// such rows.  Measured (H(div), 1024 elements): 1 row (p = 8) +4 %, 2 rows (p = 9)
+// -7 %, 3 rows (p = 10) -16 % -- the per-k-step shared-memory loads of the DFMA rows
+// cost more than the DMMA padding they save beyond one row.
+#ifndef HXG_V2_DREM
+#define HXG_V2_DREM 1
+#endif
 
 template <int S, int P, int L, int A, int B>
 __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int e, int j3)
@@ -237,12 +245,17 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
     // ---- per-CTA stage-C operand registers ---------------------------------
     constexpr int KD = pp.nh * L;
     constexpr int NKS = (KD + 3) / 4;          // B-form k-steps
-    constexpr int NMT = (n1b + 7) / 8;         // B-form row tiles
+    constexpr int NMT0 = (n1b + 7) / 8;        // B-form row tiles
+    constexpr int NREM = n1b % 8;              // rows of a partial last row tile
+    constexpr bool DREM = NMT0 > 1 && NREM > 0 && NREM <= HXG_V2_DREM;
+    constexpr int NMT = DREM ? NMT0 - 1 : NMT0;  // row tiles on DMMA
     constexpr int YQ = C::yq(A, B);            // Y-form trial factors per test function
     constexpr int KSY = (pp.nr * L + 3) / 4;   // Y-form k-steps (segments may straddle)
     constexpr int NKR = (YF || PF) ? 1 : NKS;  // register array extents
     constexpr int NYR = YF ? KSY : 1;
     double Af[NMT][NKR];
+    int Ao[DREM ? NKR : 1];  // sT offset of u_s(j1 = 0 + shb0, l(k)) for the DFMA rows
+    (void)Ao;
     double Yb[NYR];
     double Yc[NYR][YQ];
     int Yo[NYR][YQ];
@@ -260,6 +273,9 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 for (int hh = 0; hh < pp.nh; ++hh)
                     if (hh == h) fs = pp.h_fs[hh];
                 Af[mt][ks] = (k < KD && j1 < n1b) ? sT[(fs * KT + j1 + shb0) * LP + l] : 0.0;
+                if constexpr (DREM) {
+                    if (mt == 0) Ao[ks] = k < KD ? (fs * KT + shb0) * LP + l : -1;
+                }
             }
     } else {
         // k = r L + l; lane t4 of k-step ks carries k = 4 ks + t4
@@ -561,11 +577,34 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                     double d[NMT][2];
 #pragma unroll
                     for (int mt = 0; mt < NMT; ++mt) d[mt][0] = d[mt][1] = 0.0;
+                    double pr[DREM ? NREM : 1];  // DFMA rows j1 = 8 NMT + r, column ct 8 + g8
+#pragma unroll
+                    for (int r = 0; r < (DREM ? NREM : 1); ++r) pr[r] = 0.0;
 #pragma unroll
                     for (int ks = 0; ks < (HXG_V2_SKIP & 4 ? 0 : NKS); ++ks) {
                         const double bv = X[ks] * sBj[bo[ks]];
 #pragma unroll
                         for (int mt = 0; mt < NMT; ++mt) dmma_8x8x4(d[mt][0], d[mt][1], Af[mt][ks], bv);
+                        if constexpr (DREM) {
+                            if (Ao[ks] >= 0) {
+#pragma unroll
+                                for (int r = 0; r < NREM; ++r) pr[r] = fma(sT[Ao[ks] + (8 * NMT + r) * LP], bv, pr[r]);
+                            }
+                        }
+                    }
+                    if constexpr (DREM) {  // sum the four k-lanes (t4) of each column g8
+#pragma unroll
+                        for (int r = 0; r < NREM; ++r) {
+                            pr[r] += __shfl_xor_sync(0xffffffffu, pr[r], 1);
+                            pr[r] += __shfl_xor_sync(0xffffffffu, pr[r], 2);
+                        }
+                        if (t4 < NREM) {  // lane t4 stores row 8 NMT + t4
+                            double v = pr[0];
+#pragma unroll
+                            for (int r = 1; r < NREM; ++r)
+                                if (t4 == r) v = pr[r];
+                            sS[sRow[jj2 * n1b + 8 * NMT + t4] + ct * 8 + g8] = v;
+                        }
                     }
 #pragma unroll
                     for (int mt = 0; mt < NMT; ++mt) {
