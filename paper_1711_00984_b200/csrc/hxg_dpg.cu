@@ -449,15 +449,17 @@ __device__ AcBlock ac_block(int b, int pr, double omega)
 // shared memory (sOut).  The finished block is written once to each requested output:
 // its Bre or Bim part, zeros to the other part (the reference never writes those
 // blocks), and the four positions of the real block form B2 = [[Bre, -Bim], [Bim, Bre]].
-__global__ void __launch_bounds__(256) acoustics_block_kernel(int p0, int pr, int L, double omega, int c3,
+template <int P0C>  // trial order as a compile-time constant (0: runtime p0_arg)
+__global__ void __launch_bounds__(256) acoustics_block_kernel(int p0_arg, int pr, int L, double omega, int c3,
                                                              const double *__restrict__ tab,
                                                              const double *__restrict__ F,
                                                              double *__restrict__ Bre,
                                                              double *__restrict__ Bim,
                                                              double *__restrict__ B2)
 {
+    const int p0 = P0C > 0 ? P0C : p0_arg;
     extern __shared__ double sm[];
-    const int b = blockIdx.x, e = blockIdx.y;
+    const int b = blockIdx.x % 16, e = blockIdx.x / 16;  // 1D grid: E may exceed 65535
     const AcBlock B = ac_block(b, pr, omega);
     const int q = pr + 1, mw = q * q * q, mv = 3 * q * pr * pr, m = mw + mv;
     const int ny = p0 * p0 * p0, n = 4 * ny;
@@ -714,10 +716,19 @@ int hxg_acoustics_batched(int p0, int pr, double omega, int L, int E, const int 
     if (status && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
     acoustics_geom_kernel<<<grid_for((long long)E * L * L * L, 256), 256, 0, st>>>(L, E, kind, params, tables,
                                                                                   F, status);
-    if (cudaFuncSetAttribute(acoustics_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
+    auto kern = acoustics_block_kernel<0>;
+    switch (p0) {
+    case 1: kern = acoustics_block_kernel<1>; break;
+    case 2: kern = acoustics_block_kernel<2>; break;
+    case 3: kern = acoustics_block_kernel<3>; break;
+    case 4: kern = acoustics_block_kernel<4>; break;
+    case 5: kern = acoustics_block_kernel<5>; break;
+    case 6: kern = acoustics_block_kernel<6>; break;
+    default: break;
+    }
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return HXG_ERR_CUDA;
-    acoustics_block_kernel<<<dim3(16, E), 256, smem, st>>>(p0, pr, L, omega, c3, tables, F, Bre, Bim, B2);
+    kern<<<16 * E, 256, smem, st>>>(p0, pr, L, omega, c3, tables, F, Bre, Bim, B2);
     if (lre)
         acoustics_load_kernel<<<grid_for((long long)E * m, 128), 128, 0, st>>>(pr, L, E, pairing, tables, F,
                                                                              fgrid, lre);

@@ -332,3 +332,25 @@ def test_acoustics_errors():
         acoustics_ultraweak_element(UltraweakAcousticsProblem(1.0, 1.0), 0, 1, preset_map("identity"))
     s = acoustics_ultraweak_element(UltraweakAcousticsProblem(1.0, 1.0), 1, 1, preset_map("identity"))
     assert not s.l.any()
+
+
+@pytest.mark.gpu
+def test_condense_batched_chunked(orc):
+    """More elements than one workspace chunk (the C ABI works through the batch in
+    chunks of <= 512 MB of working copies): spot-check elements of every chunk."""
+    from paper_1711_00984_b200 import _native
+    from paper_1711_00984_b200.dpg import condense_batched
+
+    m, n, E = 216, 125, 700
+    lib = _native.lib()
+    per = (m + n + 1) ** 2 * 8
+    assert lib.hxg_condense_workspace_size(m, n, E) < E * per  # really chunked
+    G, B, l = _spd_systems(4, m, n, 31)
+    idx = np.arange(E) % 4
+    iu = np.triu_indices(m)
+    A, rhs, st = condense_batched(G[idx][:, iu[0], iu[1]], B[idx], l[idx])
+    assert int(st.abs().sum()) == 0
+    A, rhs = A.cpu().numpy(), rhs.cpu().numpy()
+    for e in (0, 1, 545, 546, 547, 699):
+        Ar, rr = orc.condense(G[idx[e]], B[idx[e]], l[idx[e]])
+        assert rel(A[e], Ar) <= TOL and rel(rhs[e], rr) <= TOL_RHS
