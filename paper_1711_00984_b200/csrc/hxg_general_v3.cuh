@@ -52,9 +52,10 @@ struct V3Cfg {
     }
     static constexpr int NT = maxt();
     // test digits i3 per work unit: the packed row segment of a unit is K * C12 long, so
-    // each bulk copy moves K times as many bytes (the TMA engine accepts about one small
-    // copy per ~32 SM cycles: measured ~3.4 TB/s for ~400-byte rows); HBM-bound spaces
-    // use K = 2 with one staging buffer, FP64-bound spaces K = 1 with two
+    // each bulk copy moves K times as many bytes and the issuing warp spends K times
+    // fewer copy-issue cycles (the UBLKCP waterfall) per output byte (DESIGN.md,
+    // "Write-out cost"); HBM-bound spaces use K > 1 with one staging buffer,
+    // FP64-bound spaces K = 1 with two
     // measured best of K = 1..4 (profiles/v3_k_r01.txt, sweep_r01.json): H(div) 4 at
     // p <= 4 and p = 7, 2 at p = 6, 1 at p = 5; L2 (p = 7) 4
 #ifdef HXG_V3_K_HDIV
