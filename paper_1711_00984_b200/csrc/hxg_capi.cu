@@ -275,6 +275,64 @@ int check_common(int space, int path, int p1, int p2, int p3, int L, int E)
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// extrusion path, anisotropic orders with a rule too short for xi1 (L < p1 + 1):
+// the reference integrates xi1 exactly (F tables) and (xi2, xi3) with the L-point
+// rule.  The hierarchical bases are nested, so the anisotropic Gram is the
+// sub-matrix of the isotropic order-p = max(p_d) Gram (computed by the exact
+// extrusion kernel with the same rule) on the basis functions the orders keep.
+// ---------------------------------------------------------------------------
+__device__ int ext_iso_index(int space, int r, int p1, int p2, int p3, int p)
+{
+    const int pd[3] = {p1, p2, p3};
+    if (space == H1 || space == L2) {
+        const int s = space == H1 ? 1 : 0;
+        const int q0 = pd[0] + s, q1 = pd[1] + s, Q = p + s;
+        const int i1 = r % q0, i2 = (r / q0) % q1, i3 = r / (q0 * q1);
+        return i1 + Q * (i2 + Q * i3);
+    }
+    int off = 0, offI = 0;
+    for (int a = 0; a < 3; ++a) {
+        int n[3], Nn[3];
+        for (int d = 0; d < 3; ++d) {
+            const int e = space == HDIV ? (d == a) : (d != a);
+            n[d] = pd[d] + e;
+            Nn[d] = p + e;
+        }
+        const int sz = n[0] * n[1] * n[2];
+        if (r < off + sz) {
+            const int x = r - off;
+            const int i1 = x % n[0], i2 = (x / n[0]) % n[1], i3 = x / (n[0] * n[1]);
+            return offI + i1 + Nn[0] * (i2 + Nn[1] * i3);
+        }
+        off += sz;
+        offI += Nn[0] * Nn[1] * Nn[2];
+    }
+    return -1;
+}
+
+__global__ void ext_gather_kernel(int space, int p1, int p2, int p3, int p, int N, int Niso, int E,
+                                  const double *__restrict__ iso, double *__restrict__ out)
+{
+    const long long P = (long long)N * (N + 1) / 2, Piso = (long long)Niso * (Niso + 1) / 2;
+    const int lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); row < (long long)E * N;
+         row += nw) {
+        const long long e = row / N;
+        const int r = (int)(row - e * N);
+        const int R = ext_iso_index(space, r, p1, p2, p3, p);
+        const double *src = iso + e * Piso + (long long)R * Niso - (long long)R * (R - 1) / 2 - R;
+        double *dst = out + e * P + (long long)r * N - (long long)r * (r - 1) / 2 - r;
+        for (int c = r + lane; c < N; c += 32) dst[c] = src[ext_iso_index(space, c, p1, p2, p3, p)];
+    }
+}
+
+static bool ext_gather_route(int path, int p1, int p2, int p3, int L)
+{
+    return path == EXTRUSION && !(p1 == p2 && p2 == p3) && L < p1 + 1;
+}
+
 // ===========================================================================
 // extern "C" API
 // ===========================================================================
@@ -335,6 +393,12 @@ size_t hxg_workspace_size(int space, int path, int p1, int p2, int p3, int L, in
 {
     if (check_common(space, path, p1, p2, p3, L, E) != HXG_OK) return 0;
     if (path == AFFINE || E == 0) return 0;
+    if (ext_gather_route(path, p1, p2, p3, L)) {  // isotropic order-max(p) Grams per chunk
+        const int p = std::max(p1, std::max(p2, p3));
+        if (p > 10) return 0;
+        const size_t per = sizeof(double) * (size_t)hxg_dim(space, p, p, p) * (hxg_dim(space, p, p, p) + 1) / 2;
+        return std::min<size_t>((size_t)E, std::max<size_t>(1, WS_TARGET / per)) * per;
+    }
     if (path == EXTRUSION && p1 == p2 && p2 == p3 && p1 <= 10 &&
         !(getenv("HXG_FORCE_GENERIC") && getenv("HXG_FORCE_GENERIC")[0] == '1'))
         return 0;  // specialized kernel, no metric workspace
@@ -457,6 +521,42 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
             default: r = launch_ext_l2(p1, x, st); break;
             }
             if (r <= 0) return r == 0 ? HXG_OK : HXG_ERR_CUDA;
+        }
+        if (ext_gather_route(path, p1, p2, p3, L)) {
+            const int p = std::max(p1, std::max(p2, p3));
+            if (p > 10) return HXG_ERR_ORDER;  // no exact-xi1 kernel above p = 10
+            const int N = hxg_dim(space, p1, p2, p3), Ni = hxg_dim(space, p, p, p);
+            const size_t per = sizeof(double) * (size_t)Ni * (Ni + 1) / 2;
+            if (!workspace || workspace_bytes < per) return HXG_ERR_WORKSPACE;
+            const int chunk = (int)std::min<size_t>((size_t)E, workspace_bytes / per);
+            for (int e0 = 0; e0 < E; e0 += chunk) {
+                const int ne = std::min(chunk, E - e0);
+                ExtArgs x;
+                x.kind = kind + e0;
+                x.params = params + 24LL * e0;
+                x.coef = coef ? coef + e0 : nullptr;
+                x.tables = tables;
+                x.out = (double *)workspace;
+                x.status = status + e0;
+                x.P = (long long)Ni * (Ni + 1) / 2;
+                x.E = ne;
+                x.rg = 1;
+                x.L = L;
+                x.jc = 1;
+                int r = 1;
+                switch (space) {
+                case H1: r = launch_ext_H1(p, x, st); break;
+                case HCURL: r = launch_ext_hcurl(p, x, st); break;
+                case HDIV: r = launch_ext_hdiv(p, x, st); break;
+                default: r = launch_ext_l2(p, x, st); break;
+                }
+                if (r != 0) return HXG_ERR_CUDA;
+                const long long rows = (long long)ne * N;
+                ext_gather_kernel<<<(int)std::min<long long>((rows + 7) / 8, 148LL * 64), 256, 0, st>>>(
+                    space, p1, p2, p3, p, N, Ni, ne, (const double *)workspace, out + (long long)e0 * Pk);
+                if (cudaGetLastError() != cudaSuccess) return HXG_ERR_CUDA;
+            }
+            return HXG_OK;
         }
         ext_kind_kernel<<<(E + 255) / 256, 256, 0, st>>>(E, kind, status);
         if (cudaGetLastError() != cudaSuccess) return HXG_ERR_CUDA;

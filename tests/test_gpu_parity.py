@@ -379,3 +379,15 @@ def test_extrusion_host_entry_matches_device_entry():
     get_engine().integrate_host("Hcurl", "extrusion", (4, 4, 4), 5, b.kind, b.params, b.coef, out)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(out, dev.cpu().numpy())
+
+
+@pytest.mark.parametrize("space", SPACES)
+@pytest.mark.parametrize("orders,L", [((2, 1, 1), 2), ((3, 2, 1), 2), ((4, 2, 3), 3), ((1, 3, 2), 1)])
+def test_extrusion_anisotropic_short_rule(space, orders, L, orc):
+    """Regression (found by tests/test_gpu_property.py): anisotropic orders with a rule
+    shorter than p1 + 1 on the extrusion path -- xi1 must still be integrated exactly
+    (simp_*_ext uses F tables in xi1), only (xi2, xi3) use the L-point rule."""
+    from paper_1711_00984_b200.inputs import extrusion_batch
+
+    b = extrusion_batch(4, 900 + L + sum(orders), variable_coef=True)
+    check_batch(space, "extrusion", orders, L, b, orc)
