@@ -57,8 +57,10 @@ static int launch_one(const V2Args &a, int grid, cudaStream_t st)
             b.coef = a.coef;
             b.wgrid = a.wgrid;
             b.status = a.status;
+            // one element per item once the batch fills a wave of CTAs: the warps then
+            // flow from element to element (general_v3_kernel, HXG_V3_FLOW)
             const int want = 148 * C3::MINB * 2;
-            b.split = a.E >= want ? 1 : (want + a.E - 1) / a.E;
+            b.split = a.E >= 148 * C3::MINB ? 1 : (want + a.E - 1) / a.E;
             if (b.split > 16) b.split = 16;
             if (getenv("HXG_V3_SPLIT")) b.split = atoi(getenv("HXG_V3_SPLIT"));
             // persistent CTAs (grid-stride over (element, part) items)
