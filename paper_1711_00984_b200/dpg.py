@@ -180,9 +180,10 @@ def condense_batched(G, B, l=None, *, device=None, stream=None, check: bool = Tr
     rhs = torch.empty((E, n), dtype=torch.float64, device=dev)
     status = torch.zeros(E, dtype=torch.int32, device=dev)
     ws_bytes = eng.lib.hxg_condense_workspace_size(m, n, max(E, 1))
-    ws = eng.workspace(ws_bytes)
-    rc = eng.lib.hxg_condense_batched(m, n, E, _vp(G), _vp(B), _vp(l), _vp(A), _vp(rhs),
-                                      _vp(status), _vp(ws), ws_bytes, sp)
+    with eng._lock:
+        ws = eng.workspace(ws_bytes, st)
+        rc = eng.lib.hxg_condense_batched(m, n, E, _vp(G), _vp(B), _vp(l), _vp(A), _vp(rhs),
+                                          _vp(status), _vp(ws), ws_bytes, sp)
     _check(rc, "hxg_condense_batched")
     if check:
         bad = torch.nonzero(status).flatten()
@@ -291,10 +292,12 @@ def acoustics_batched(p0: int, pr: int, omega: float, kind, params, fgrid=None, 
     status = torch.zeros(E, dtype=torch.int32, device=dev)
     tab = eng.tables(L, stream=st)
     ws_bytes = eng.lib.hxg_acoustics_workspace_size(p0, pr, L, E)
-    ws = eng.workspace(ws_bytes)
-    rc = eng.lib.hxg_acoustics_batched(p0, pr, float(omega), L, E, _vp(kind), _vp(params), _vp(tab),
-                                       _vp(fgrid), 0 if pairing == "velocity" else 1, _vp(Bre),
-                                       _vp(Bim), _vp(B2), _vp(lre), _vp(status), _vp(ws), ws_bytes, sp)
+    with eng._lock:
+        ws = eng.workspace(ws_bytes, st)
+        rc = eng.lib.hxg_acoustics_batched(p0, pr, float(omega), L, E, _vp(kind), _vp(params),
+                                           _vp(tab), _vp(fgrid), 0 if pairing == "velocity" else 1,
+                                           _vp(Bre), _vp(Bim), _vp(B2), _vp(lre), _vp(status),
+                                           _vp(ws), ws_bytes, sp)
     _check(rc, "hxg_acoustics_batched")
     return Bre, Bim, B2, lre, status
 

@@ -45,7 +45,7 @@ class GramEngine:
             self.device = torch.device("cuda", torch.cuda.current_device())
         self.lib = _native.lib()
         self._tables = {}
-        self._ws = None
+        self._ws = {}
         self._lock = threading.Lock()
 
     # -- 1D tables ---------------------------------------------------------
@@ -69,12 +69,17 @@ class GramEngine:
         self._tables[key] = t
         return t
 
-    def workspace(self, nbytes: int) -> torch.Tensor:
+    def workspace(self, nbytes: int, stream=None) -> torch.Tensor:
+        """Scratch buffer of at least `nbytes`, one per stream: calls are stream-ordered,
+        so reuse on the same stream is safe and distinct streams never share one."""
         if nbytes == 0:
             return None
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        return self._ws
+        key = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        return ws
 
     # -- batched integration -------------------------------------------------
     def integrate(self, space: str, path: str, orders, L: int, kind, params, coef=None,
@@ -107,7 +112,7 @@ class GramEngine:
         tab = self.tables(L if path == "general" else max(L, 1), nodes, weights, st)
         with self._lock:
             ws_bytes = self.lib.hxg_workspace_size(sc, pc, p1, p2, p3, L, E)
-            ws = self.workspace(ws_bytes)
+            ws = self.workspace(ws_bytes, st)
             rc = self.lib.hxg_gram_batched(sc, pc, p1, p2, p3, L, E, _ptr(kind), _ptr(params),
                                            _ptr(coef), _ptr(wgrid), _ptr(tab), _ptr(out),
                                            _ptr(status), _ptr(ws), ws_bytes,
