@@ -104,12 +104,13 @@ __device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2lo, int 
     const double *sAb = smem + C::off_abar(L) + (size_t)A * N3 * NG * L;
     // a thread owns (j2, i2) and up to C3 digits i3: the factor u(i2, m) u(j2, m) of
     // each group is formed once and reused for its i3 digits (it does not depend on i3).
-    // Measured (x5 sweep points, 8192 elements): C3 = 4 +8 % for H(div) (few groups);
-    // H1 / H(curl) (up to 9 groups) lose occupancy to the accumulators, C3 = 1 there.
+    // Measured (config-5 sweep): C3 = 4 lifts H(div) at p >= 6 (75-95 % vs 69-90 %) but
+    // starves p <= 5 of thread items; H1 / H(curl) (up to 9 groups) lose occupancy to
+    // the accumulators: C3 = 1 there.
 #ifdef HXG_EXT_C3
     constexpr int C3 = HXG_EXT_C3;
 #else
-    constexpr int C3 = S == HDIV ? 4 : 1;
+    constexpr int C3 = (S == HDIV && P >= 6) ? 4 : 1;
 #endif
     constexpr int NCI = (n3a + C3 - 1) / C3;
     constexpr int LV = LC ? LC : LT;
