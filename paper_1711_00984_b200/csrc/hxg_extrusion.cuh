@@ -112,6 +112,27 @@ __device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2lo, int 
 #else
     constexpr int C3 = (S == HDIV && P >= 6) ? 4 : 1;
 #endif
+    if constexpr (C3 == 1) {
+    for (int it = threadIdx.x; it < jn * n2a * n3a; it += AFF2_THREADS) {
+        const int jj = it / (n2a * n3a), k = it - jj * (n2a * n3a), j2 = j2lo + jj;
+        const int i2 = k % n2a, i3 = k / n2a;
+        double acc[MAXH] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int g = 0; g < pp.ng; ++g) {
+            const double *Ta = sT + (pp.g_fr[g] * KT + i2 + sa1) * LT;
+            const double *Tb = sT + (pp.g_fs[g] * KT + j2 + sb1) * LT;
+            const double *Ab = sAb + (i3 * NG + g) * L;
+            double s = 0.0;
+#pragma unroll
+            for (int m = 0; m < (LC ? LC : LT); ++m)
+                if (LC || m < L) s = fma(Ta[m] * Tb[m], Ab[m], s);
+            acc[pp.g_h[g]] += s;
+        }
+        double2 *dst = reinterpret_cast<double2 *>(smem + C::off_bs(L) + jj * C::BS_SLOT + (A * C::NK + k) * 4);
+        dst[0] = make_double2(acc[0], acc[1]);
+        dst[1] = make_double2(acc[2], acc[3]);
+    }
+    } else {
     constexpr int NCI = (n3a + C3 - 1) / C3;
     constexpr int LV = LC ? LC : LT;
     for (int it = threadIdx.x; it < jn * n2a * NCI; it += AFF2_THREADS) {
@@ -151,6 +172,7 @@ __device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2lo, int 
                 dst[1] = make_double2(acc[c][2], acc[c][3]);
             }
         }
+    }
     }
 }
 
