@@ -146,9 +146,14 @@ __global__ void graph_assemble_kernel(int mw, int mv, int E, const double *__res
 // Mt = m + n + 1.  Working copy: dense row-major lower triangle per element
 // in the workspace (rows i >= j only).
 // ---------------------------------------------------------------------------
-constexpr int CD_THREADS = 256;
-constexpr int CD_NB = 32;  // panel width
-constexpr int CD_TT = 64;  // trailing-update tile (CD_THREADS threads x 4 x 4)
+#ifndef HXG_CD_WARPS
+#define HXG_CD_WARPS 8
+#endif
+constexpr int CD_WARPS = HXG_CD_WARPS;
+constexpr int CD_THREADS = 32 * CD_WARPS;
+constexpr int CD_NB = 32;            // panel width
+constexpr int CD_TT = 8 * CD_WARPS;  // trailing-update tile (rows of the panel solve: 8 per warp)
+constexpr int CD_NBC = CD_TT / 16;   // 8-column DMMA tiles per warp in the trailing update
 
 __global__ void condense_init_kernel(int m, int n, int Ec, const double *__restrict__ G,
                                      const double *__restrict__ B, const double *__restrict__ l,
@@ -181,7 +186,7 @@ __device__ __forceinline__ void cd_dmma(double &d0, double &d1, double a, double
 
 constexpr int CD_PS = CD_NB + 4;  // panel row stride (doubles): 8-byte fragment loads hit 16 distinct banks
 
-// One CTA (8 warps) per element.  Per panel of CD_NB columns:
+// One CTA (CD_WARPS warps) per element.  Per panel of CD_NB columns:
 //   (a) warp 0 factors the diagonal block L_D (unblocked, shared memory) and forms
 //       L_D^-1 (one column per lane);
 //   (b) per 64-row tile ti of the rows below: X = P L_D^-T as a DMMA product with the
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                 const int rr = idx / CD_NB, t = idx - rr * CD_NB;
                 if (t < kb && ib + rr < Mt) W[(long long)(ib + rr) * Mt + k0 + t] = sPi[rr][t];
             }
-            // (c) trailing update, warp w: rows 16 (w >> 1) .. +16, columns 32 (w & 1) .. +32
+            // (c) trailing update, warp w: rows 16 (w >> 1) .. +16, columns (CD_TT / 2) (w & 1) .. + CD_TT / 2
             const int rb = warp >> 1, cb = warp & 1;
             for (int tj = 0; tj <= ti; ++tj) {
                 const int jb = r0 + tj * CD_TT;
@@ -296,25 +301,25 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                 __syncthreads();
                 double(*Pj)[CD_PS] = tj < ti ? sPj : sPi;
                 // skip warp tiles entirely above the diagonal of a diagonal tile
-                const bool live = !(tj == ti && 32 * cb > 16 * rb + 15);
+                const bool live = !(tj == ti && (CD_TT / 2) * cb > 16 * rb + 15);
                 if (live) {
-                    double acc[2][4][2];
+                    double acc[2][CD_NBC][2];
 #pragma unroll
                     for (int a = 0; a < 2; ++a)
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+                        for (int b = 0; b < CD_NBC; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll
                     for (int ks = 0; ks < CD_NB / 4; ++ks) {
                         const int t = 4 * ks + t4;
-                        double av[2], bv[4];
+                        double av[2], bv[CD_NBC];
 #pragma unroll
                         for (int a = 0; a < 2; ++a) av[a] = sPi[16 * rb + 8 * a + g8][t];
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) bv[b] = Pj[32 * cb + 8 * b + g8][t];
+                        for (int b = 0; b < CD_NBC; ++b) bv[b] = Pj[(CD_TT / 2) * cb + 8 * b + g8][t];
 #pragma unroll
                         for (int a = 0; a < 2; ++a)
 #pragma unroll
-                            for (int b = 0; b < 4; ++b) cd_dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+                            for (int b = 0; b < CD_NBC; ++b) cd_dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
                     }
 #pragma unroll
                     for (int a = 0; a < 2; ++a) {
@@ -322,8 +327,8 @@ __global__ void __launch_bounds__(CD_THREADS) condense_kernel(int m, int n, doub
                         if (i >= Mt) continue;
                         double *Wi = W + (long long)i * Mt;
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            const int j = jb + 32 * cb + 8 * b + 2 * t4;
+                        for (int b = 0; b < CD_NBC; ++b) {
+                            const int j = jb + (CD_TT / 2) * cb + 8 * b + 2 * t4;
                             if (j <= i) Wi[j] -= acc[a][b][0];
                             if (j + 1 <= i) Wi[j + 1] -= acc[a][b][1];
                         }
