@@ -34,6 +34,10 @@ struct ExtArgs {
     int jc;  // trial digits j2 whose Bs sums are built per pass (host: smem budget)
 };
 
+#ifndef HXG_EXT_VT
+#define HXG_EXT_VT 1
+#endif
+
 template <int S, int P>
 struct ExtCfg {
     using A = AffCfg<S, P>;
@@ -56,7 +60,22 @@ struct ExtCfg {
     __host__ __device__ static constexpr int off_abar(int L) { return OFF_M + NF * L * L; }
     __host__ __device__ static constexpr int off_bs(int L) { return (off_abar(L) + NB * N3 * NG * L + 1) & ~1; }  // double2
     static constexpr int BS_SLOT = NB * NK * 4;  // Bs of one j2, every test block
-    __host__ __device__ static constexpr int smem_bytes(int L, int jc) { return (off_bs(L) + jc * BS_SLOT) * 8; }
+    // stage-B factor table Vt[jj][fr 2 + fs][ra][m] = u_fr(ra, m) u_fs(j2 + sb1, m) of the
+    // current j2 chunk (HXG_EXT_VT): formed once per chunk instead of per (i2, i3, g) item
+    static constexpr int KF = A::KF;
+    // stage-B digits i3 per thread item (see ext_stage_b); the Vt table serves C3 == 1
+#ifdef HXG_EXT_C3
+    static constexpr int C3 = HXG_EXT_C3;
+#else
+    static constexpr int C3 = (S == HDIV && P >= 6) ? 4 : 1;
+#endif
+    static constexpr bool VT = HXG_EXT_VT && C3 == 1;
+    __host__ __device__ static constexpr int vt_slot(int L) { return VT ? 4 * KF * L : 0; }
+    __host__ __device__ static constexpr int off_vt(int L, int jc) { return off_bs(L) + jc * BS_SLOT; }
+    __host__ __device__ static constexpr int smem_bytes(int L, int jc)
+    {
+        return (off_vt(L, jc) + jc * vt_slot(L)) * 8;
+    }
 };
 
 // stage A for test block A of the (A, B) pair: Abar[A][i3][g][m]
@@ -93,7 +112,7 @@ __device__ __forceinline__ void ext_stage_a(double *smem, int Lr, int j3)
 
 // stage B for test block A of the (A, B) pair: Bs_h[A][k = i2 + n2a i3][h]
 template <int S, int P, int LC, int A, int B>
-__device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2lo, int jn)
+__device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2lo, int jn, int jc)
 {
     using C = ExtCfg<S, P>;
     constexpr CPair pp = make_pair_plan(S, A, B);
@@ -107,25 +126,30 @@ __device__ __forceinline__ void ext_stage_b(double *smem, int Lr, int j2lo, int 
     // Measured (config-5 sweep): C3 = 4 lifts H(div) at p >= 6 (75-95 % vs 69-90 %) but
     // starves p <= 5 of thread items; H1 / H(curl) (up to 9 groups) lose occupancy to
     // the accumulators: C3 = 1 there.
-#ifdef HXG_EXT_C3
-    constexpr int C3 = HXG_EXT_C3;
-#else
-    constexpr int C3 = (S == HDIV && P >= 6) ? 4 : 1;
-#endif
+    constexpr int C3 = C::C3;
     if constexpr (C3 == 1) {
+    const double *sVt = smem + C::off_vt(L, jc);
+    (void)sVt;
     for (int it = threadIdx.x; it < jn * n2a * n3a; it += AFF2_THREADS) {
         const int jj = it / (n2a * n3a), k = it - jj * (n2a * n3a), j2 = j2lo + jj;
         const int i2 = k % n2a, i3 = k / n2a;
         double acc[MAXH] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < pp.ng; ++g) {
-            const double *Ta = sT + (pp.g_fr[g] * KT + i2 + sa1) * LT;
-            const double *Tb = sT + (pp.g_fs[g] * KT + j2 + sb1) * LT;
             const double *Ab = sAb + (i3 * NG + g) * L;
             double s = 0.0;
+            if constexpr (C::VT) {
+                const double *V = sVt + ((jj * 4 + pp.g_fr[g] * 2 + pp.g_fs[g]) * C::KF + i2 + sa1) * L;
 #pragma unroll
-            for (int m = 0; m < (LC ? LC : LT); ++m)
-                if (LC || m < L) s = fma(Ta[m] * Tb[m], Ab[m], s);
+                for (int m = 0; m < (LC ? LC : LT); ++m)
+                    if (LC || m < L) s = fma(V[m], Ab[m], s);
+            } else {
+                const double *Ta = sT + (pp.g_fr[g] * KT + i2 + sa1) * LT;
+                const double *Tb = sT + (pp.g_fs[g] * KT + j2 + sb1) * LT;
+#pragma unroll
+                for (int m = 0; m < (LC ? LC : LT); ++m)
+                    if (LC || m < L) s = fma(Ta[m] * Tb[m], Ab[m], s);
+            }
             acc[pp.g_h[g]] += s;
         }
         double2 *dst = reinterpret_cast<double2 *>(smem + C::off_bs(L) + jj * C::BS_SLOT + (A * C::NK + k) * 4);
@@ -201,19 +225,35 @@ __device__ __forceinline__ void ext_stage_a_all(double *smem, int L, int b, int 
 }
 
 template <int S, int P, int LC>
-__device__ __forceinline__ void ext_stage_b_all(double *smem, int L, int b, int j2lo, int jn)
+__device__ __forceinline__ void ext_stage_b_all(double *smem, int L, int b, int j2lo, int jn, int jc)
 {
     if constexpr (ExtCfg<S, P>::NB == 1) {
-        ext_stage_b<S, P, LC, 0, 0>(smem, L, j2lo, jn);
+        ext_stage_b<S, P, LC, 0, 0>(smem, L, j2lo, jn, jc);
     } else if (b == 0) {
-        ext_stage_b<S, P, LC, 0, 0>(smem, L, j2lo, jn);
-        ext_stage_b<S, P, LC, 1, 0>(smem, L, j2lo, jn);
-        ext_stage_b<S, P, LC, 2, 0>(smem, L, j2lo, jn);
+        ext_stage_b<S, P, LC, 0, 0>(smem, L, j2lo, jn, jc);
+        ext_stage_b<S, P, LC, 1, 0>(smem, L, j2lo, jn, jc);
+        ext_stage_b<S, P, LC, 2, 0>(smem, L, j2lo, jn, jc);
     } else if (b == 1) {
-        ext_stage_b<S, P, LC, 1, 1>(smem, L, j2lo, jn);
-        ext_stage_b<S, P, LC, 2, 1>(smem, L, j2lo, jn);
+        ext_stage_b<S, P, LC, 1, 1>(smem, L, j2lo, jn, jc);
+        ext_stage_b<S, P, LC, 2, 1>(smem, L, j2lo, jn, jc);
     } else {
-        ext_stage_b<S, P, LC, 2, 2>(smem, L, j2lo, jn);
+        ext_stage_b<S, P, LC, 2, 2>(smem, L, j2lo, jn, jc);
+    }
+}
+
+// Vt of the j2 chunk [j2lo, j2lo + jn) for trial block b (written while no one reads it)
+template <int S, int P>
+__device__ __forceinline__ void ext_build_vt(double *smem, int L, int b, int j2lo, int jn, int jc)
+{
+    using C = ExtCfg<S, P>;
+    if constexpr (C::VT) {
+        const double *sT = smem + C::OFF_T;
+        double *sVt = smem + C::off_vt(L, jc);
+        const int sb1 = sh_of(S, b, 1);
+        for (int idx = threadIdx.x; idx < jn * 4 * C::KF * L; idx += AFF2_THREADS) {
+            const int m = idx % L, q = idx / L, ra = q % C::KF, q2 = q / C::KF, combo = q2 & 3, jj = q2 >> 2;
+            sVt[idx] = sT[((combo >> 1) * KT + ra) * LT + m] * sT[((combo & 1) * KT + j2lo + jj + sb1) * LT + m];
+        }
     }
 }
 
@@ -284,16 +324,19 @@ __global__ void __launch_bounds__(AFF2_THREADS) ext_v2_kernel(const __grid_const
 #pragma unroll
         for (int bb = 1; bb < C::NB; ++bb)
             if (b == bb) n2b = C::n(bb, 1);
-        __syncthreads();  // fields ready; previous slab done with Abar / Bs
+        __syncthreads();  // fields ready; previous slab done with Abar / Bs / Vt
         ext_stage_a_all<S, P, LC>(smem, L, b, j3);
+        ext_build_vt<S, P>(smem, L, b, 0, cmin(args.jc, n2b), args.jc);
         for (int j2lo = 0; j2lo < n2b; j2lo += args.jc) {
             const int jn = cmin(args.jc, n2b - j2lo);
-            __syncthreads();  // Abar complete; previous rows done with the Bs slots
-            ext_stage_b_all<S, P, LC>(smem, L, b, j2lo, jn);
+            __syncthreads();  // Abar / Vt complete; previous rows done with the Bs slots
+            ext_stage_b_all<S, P, LC>(smem, L, b, j2lo, jn, args.jc);
             __syncthreads();
             const int off = C::off_bs(L) - CA::OFF_B;  // aff_rows reads OFF_B + off + slot
             for (int jj = 0; jj < jn; ++jj)
                 ext_rows_all<S, P>(smem, outE, b, j2lo + jj, j3, off + jj * C::BS_SLOT);
+            if (j2lo + args.jc < n2b)  // stage B of this chunk is done with Vt
+                ext_build_vt<S, P>(smem, L, b, j2lo + args.jc, cmin(args.jc, n2b - j2lo - args.jc), args.jc);
         }
     }
 }
@@ -308,7 +351,8 @@ inline int launch_ext_t(const ExtArgs &a, cudaStream_t st)
     const int n2max = C::A::nmax(1);
     long long budget = 24LL * 1024;
     if (const char *t = getenv("HXG_EXT_SMEM_KB")) budget = 1024LL * atoll(t);  // tuning
-    int jc = (int)std::min<long long>(n2max, std::max<long long>(1, (budget / 8 - C::off_bs(a.L)) / C::BS_SLOT));
+    int jc = (int)std::min<long long>(
+        n2max, std::max<long long>(1, (budget / 8 - C::off_bs(a.L)) / (C::BS_SLOT + C::vt_slot(a.L))));
     const size_t smem = C::smem_bytes(a.L, jc);
     if (smem > 200 * 1024) return 1;
     // the reference's default rule (L = p + 1) unrolls; other rules loop
