@@ -175,10 +175,8 @@ __global__ void __launch_bounds__(AFF2_THREADS) affine_v2_kernel(const __grid_co
         dev_jacobian(args.kind[e], args.params + 24LL * e, 0.5, 0.5, 0.5, J);
         const double det = dev_metrics(J, D, Cm);
         dev_fields(S, det, D, Cm, 1.0, args.coef ? args.coef[e] : 1.0, s_field);
-        if (cta == 0) {
-            if (!(det > 0.0)) atomicOr(args.status + e, 1);
-            if (args.kind[e] > 2) atomicOr(args.status + e, 2);  // gram.py:170-174
-        }
+        if (cta == 0)  // the element's whole status word (no zero-fill pass before the kernel)
+            args.status[e] = (det > 0.0 ? 0 : 1) | (args.kind[e] > 2 ? 2 : 0);  // gram.py:170-174
     }
     double *__restrict__ outE = args.out + (long long)e * args.P;
     const int u1 = cmin(C::NU, (cta + 1) * args.rg);

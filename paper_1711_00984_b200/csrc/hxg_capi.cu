@@ -425,10 +425,14 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
     rc = build_plan(space, p1, p2, p3, P);
     if (rc != HXG_OK) return rc;
     const long long Pk = (long long)P.N * (P.N + 1) / 2;
-    if (cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
+    // every kernel but the specialized affine one ORs flags into a zeroed status word
+    const char *force_generic = getenv("HXG_FORCE_GENERIC");
+    const bool aff_spec = path == AFFINE && p1 == p2 && p2 == p3 && p1 <= 10 &&
+                          !(force_generic && force_generic[0] == '1');
+    if (!aff_spec && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
 
     if (path == AFFINE) {
-        const char *force = getenv("HXG_FORCE_GENERIC");
+        const char *force = force_generic;
         if (p1 == p2 && p2 == p3 && !(force && force[0] == '1')) {
             // compile-time specialized kernel (isotropic p <= 10), chunked below 2^31 blocks
             const long long units = P.nb == 1 ? (long long)P.n[0][1] * P.n[0][2]
@@ -454,6 +458,8 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
                 }
             }
             if (r <= 0) return r == 0 ? HXG_OK : HXG_ERR_CUDA;
+            if (aff_spec && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess)
+                return HXG_ERR_CUDA;  // no specialization after all: the generic kernel ORs flags
         }
         AffArgs a;
         memset(&a, 0, sizeof(a));
