@@ -203,6 +203,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 #ifndef HXG_V2_AREG
 #define HXG_V2_AREG 1
 #endif
+#ifndef HXG_V2_PF_RT
+#define HXG_V2_PF_RT 2
+#endif
 #ifndef HXG_V2_PF_MINNH
 #define HXG_V2_PF_MINNH 3
 #endif
@@ -485,7 +488,8 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 // columns (2 t4, 2 t4 + 1) share j1 and sit next to each other in staging
                 constexpr int N1E = (n1a + 1) & ~1, NCOL = n1b * N1E, NCT = (NCOL + 7) / 8;
                 const int nrow = r2 * r3 * n2a, nrt = (nrow + 7) >> 3;
-                const int nrtp = (nrt + 1) >> 1;  // row-tile pairs per column tile
+                constexpr int RT = HXG_V2_PF_RT;  // row tiles in flight per warp
+                const int nrtp = (nrt + RT - 1) / RT;  // row-tile groups per column tile
                 const int T = NCT * nrtp;
                 const int per = (T + V2_WARPS - 1) / V2_WARPS;
                 const int it0 = warp * per, it1 = cmin(T, it0 + per);
@@ -493,7 +497,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 int ko[NKS];
                 int ctc = -1, dj1 = -1, di1 = 0;
                 for (int it = it0; it < it1; ++it) {
-                    const int ct = it / nrtp, rt0 = 2 * (it - ct * nrtp);
+                    const int ct = it / nrtp, rt0 = RT * (it - ct * nrtp);
                     if (ct != ctc) {  // (re)load the B fragment of column tile ct
                         ctc = ct;
                         const int col = ct * 8 + g8;
@@ -518,10 +522,12 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                             di1 = oc - (oc / N1E) * N1E;
                         }
                     }
-                    double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-                    int ao[2], jr[2], sc[2];
+                    double d[RT][2];
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {  // this lane's row g8 of row tile rt0 + c
+                    for (int c = 0; c < RT; ++c) d[c][0] = d[c][1] = 0.0;
+                    int ao[RT], jr[RT], sc[RT];
+#pragma unroll
+                    for (int c = 0; c < RT; ++c) {  // this lane's row g8 of row tile rt0 + c
                         const int row = (rt0 + c) * 8 + g8;
                         const bool rv = row < nrow;
                         const int i2 = rv ? row % n2a : 0, q = rv ? row / n2a : 0;
@@ -533,11 +539,11 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
 #pragma unroll
                     for (int ks = 0; ks < (HXG_V2_SKIP & 4 ? 0 : NKS); ++ks) {
 #pragma unroll
-                        for (int c = 0; c < 2; ++c) dmma_8x8x4(d[c][0], d[c][1], sB[ao[c] + ko[ks]], Bp[ks]);
+                        for (int c = 0; c < RT; ++c) dmma_8x8x4(d[c][0], d[c][1], sB[ao[c] + ko[ks]], Bp[ks]);
                     }
                     if (dj1 >= 0 && !(HXG_V2_SKIP & 16)) {
 #pragma unroll
-                        for (int c = 0; c < 2; ++c) {
+                        for (int c = 0; c < RT; ++c) {
                             if (jr[c] < 0) continue;
                             double *dst = sS + sRow[jr[c] + dj1] + sc[c] + di1;
                             dst[0] = d[c][0];
