@@ -63,7 +63,9 @@ enum {
     HXG_ERR_KIND = -3,         /* SimplificationNotApplicableError (gram.py:171-174)       */
     HXG_ERR_WORKSPACE = -4,    /* workspace too small                                      */
     HXG_ERR_CUDA = -5,         /* CUDA launch / runtime error                              */
-    HXG_ERR_ARG = -6           /* NULL pointer or negative count                           */
+    HXG_ERR_ARG = -6,          /* NULL pointer or negative count                           */
+    HXG_ERR_DEGENERATE = -7    /* host entry: an element has det J <= 0 (DegenerateMapError,
+                                  errors.py:12-20)                                          */
 };
 
 #define HXG_MAX_ORDER 12   /* poly1d.py:37 DEFAULT_P_MAX, cli.py:55 MAX_SUPPORTED_ORDER */
@@ -116,13 +118,27 @@ int hxg_metric_batched(int space, int p1, int p2, int p3, int L, int E, const in
 int hxg_contract_batched(int space, int p1, int p2, int p3, int L, int E, const double *tables,
                          const double *metric, double *out, void *stream);
 
-/* Same computation with HOST inputs and HOST output (the reference's
- * calling convention: numpy in, numpy out).  Copies inputs in, integrates in
- * device-sized chunks and streams the packed triangles back, overlapping the
- * device->host copies with the next chunk's integration.  `out` should be
- * page-locked for full copy bandwidth.  status may be NULL.  Synchronous. */
+/* Same computation with HOST inputs and HOST output: the reference's calling
+ * convention at the kernel seam gram.py:154-157,
+ *     kern(p1, p2, p3, rule1d.nodes, rule1d.weights, kind, params, wgrid)
+ * (numpy in, numpy out), batched over E elements.  Copies the inputs in,
+ * integrates in device-sized chunks and streams the packed triangles back,
+ * overlapping the device->host copies with the next chunk's integration.
+ *   nodes, weights : host [L] 1D rule on (0,1) (a user Rule1D), or both NULL for
+ *                    the L-point Gauss rule (quadrature.py:47-66); ignored on path 1
+ *   coef           : host [E] constant mass weights, or NULL (= 1)
+ *   wgrid          : host [E][L][L][L] mass weight sampled at the tensor nodes
+ *                    (gram.py:78-90, a callable mass_weight), or NULL; general path
+ *                    only (the simplified paths take constants, gram.py:93-98:
+ *                    HXG_ERR_ARG otherwise); overrides coef
+ *   out            : host [E][N(N+1)/2]; page-locked for full copy bandwidth
+ *   status         : host [E] or NULL; per-element flags as hxg_gram_batched
+ * Synchronous.  Like the reference, which raises before returning a matrix, a
+ * flagged element makes the call return HXG_ERR_KIND (bit 1) or
+ * HXG_ERR_DEGENERATE (bit 0) -- whether or not `status` is given. */
 int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, int E,
-                          const int *kind, const double *params, const double *coef,
+                          const double *nodes, const double *weights, const int *kind,
+                          const double *params, const double *coef, const double *wgrid,
                           double *out, int *status);
 
 /* Expand packed upper triangles [E][N(N+1)/2] into full symmetric

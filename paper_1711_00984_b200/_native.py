@@ -12,7 +12,9 @@ import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libhexgram_b200.so")
+# HXG_LIB selects an alternative build of the same library (investigation
+# builds with different compile flags, tools/v3p7_check.sh); default: in-tree
+LIB_PATH = os.environ.get("HXG_LIB") or os.path.join(LIB_DIR, "libhexgram_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 HXG_OK = 0
@@ -22,8 +24,19 @@ HXG_ERR_KIND = -3
 HXG_ERR_WORKSPACE = -4
 HXG_ERR_CUDA = -5
 HXG_ERR_ARG = -6
+HXG_ERR_DEGENERATE = -7
 HXG_MAX_ORDER = 12
 HXG_MAX_RULE = 16
+
+# device 1D-table block layout (doubles; hxg_plan.h): nodes [LT], weights [LT],
+# T[f][k][l] (f 0 chi, 1 chi') [2][KT][LT], F[rs][i][j] [4][KT][KT]
+KT = 16
+LT = 16
+TAB_NODES = 0
+TAB_WTS = TAB_NODES + LT
+TAB_T = TAB_WTS + LT
+TAB_F = TAB_T + 2 * KT * LT
+TAB_TOTAL = TAB_F + 4 * KT * KT
 
 SPACE_CODES = {"H1": 0, "Hcurl": 1, "Hdiv": 2, "L2": 3}
 PATH_CODES = {"general": 0, "affine": 1, "extrusion": 2}
@@ -95,7 +108,8 @@ def lib():
     L.hxg_metric_batched.restype = _i
     L.hxg_contract_batched.argtypes = [_i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp]
     L.hxg_contract_batched.restype = _i
-    L.hxg_gram_batched_host.argtypes = [_i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]
+    L.hxg_gram_batched_host.argtypes = [_i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                        _vp]
     L.hxg_gram_batched_host.restype = _i
     L.hxg_expand_full.argtypes = [_i, _i, _vp, _vp, _vp]
     L.hxg_expand_full.restype = _i

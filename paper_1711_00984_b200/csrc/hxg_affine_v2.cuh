@@ -10,6 +10,7 @@
 #pragma once
 #include <cstdlib>
 #include "hxg_common.cuh"
+#include "hxg_device.h"
 #include "hxg_general_v2.cuh"
 #include "hxg_geom.cuh"
 #include "hxg_terms.h"
@@ -40,7 +41,7 @@ inline int aff_row_groups(int NU, long long P, int E)
     const double per_group = 8.0 * (double)P / NU;  // mean output bytes of one row group
     long long rg = per_group >= 32768.0 ? 1 : (long long)(target / per_group);
     rg = rg < 1 ? 1 : (rg > NU ? NU : rg);
-    while (rg > 1 && (long long)E * ((NU + rg - 1) / rg) < 148LL * 16) rg = (rg + 1) / 2;
+    while (rg > 1 && (long long)E * ((NU + rg - 1) / rg) < (long long)sm_count() * 16) rg = (rg + 1) / 2;
     if (const char *r = getenv("HXG_AFF_RG")) rg = atoi(r) < 1 ? 1 : (atoi(r) > NU ? NU : atoi(r));  // tuning
     return (int)rg;
 }

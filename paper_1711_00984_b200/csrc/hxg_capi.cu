@@ -11,6 +11,7 @@
 #include "hxg_affine_v2.cuh"
 #include "hxg_extrusion.cuh"
 #include "hxg_general_v2.cuh"
+#include "hxg_device.h"
 #include "hxg_kernels.cuh"
 #include "hxg_v2_launch.h"
 #include <cstdlib>
@@ -333,6 +334,24 @@ static bool ext_gather_route(int path, int p1, int p2, int p3, int L)
     return path == EXTRUSION && !(p1 == p2 && p2 == p3) && L < p1 + 1;
 }
 
+static int metric_run(int space, int p1, int p2, int p3, int L, int E, const int *kind,
+                       const double *params, const double *coef, const double *wgrid,
+                       const double *tables, double *metric, int *status, void *stream)
+{
+    int rc = check_common(space, GENERAL, p1, p2, p3, L, E);
+    if (rc != HXG_OK) return rc;
+    if (E == 0) return HXG_OK;
+    if (!kind || !params || !tables || !metric || !status) return HXG_ERR_ARG;
+    SpacePlan P;
+    rc = build_plan(space, p1, p2, p3, P);
+    if (rc != HXG_OK) return rc;
+    const long long npts = (long long)E * L * L * L;
+    const int mgrid = (int)std::min<long long>((npts + 255) / 256, (long long)sm_count() * 64);
+    metric_kernel<<<mgrid, 256, 0, (cudaStream_t)stream>>>(space, L, E, kind, params, coef, wgrid,
+                                                         tables, metric, status, P.nfields);
+    return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
+}
+
 // ===========================================================================
 // extern "C" API
 // ===========================================================================
@@ -350,6 +369,7 @@ const char *hxg_error_string(int code)
     case HXG_ERR_WORKSPACE: return "workspace too small";
     case HXG_ERR_CUDA: return "CUDA error";
     case HXG_ERR_ARG: return "invalid argument";
+    case HXG_ERR_DEGENERATE: return "element map with det J <= 0 at a quadrature point";
     }
     return "unknown error";
 }
@@ -558,7 +578,7 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
                 }
                 if (r != 0) return HXG_ERR_CUDA;
                 const long long rows = (long long)ne * N;
-                ext_gather_kernel<<<(int)std::min<long long>((rows + 7) / 8, 148LL * 64), 256, 0, st>>>(
+                ext_gather_kernel<<<(int)std::min<long long>((rows + 7) / 8, (long long)sm_count() * 64), 256, 0, st>>>(
                     space, p1, p2, p3, p, N, Ni, ne, (const double *)workspace, out + (long long)e0 * Pk);
                 if (cudaGetLastError() != cudaSuccess) return HXG_ERR_CUDA;
             }
@@ -602,7 +622,7 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
     for (long long e0 = 0; e0 < E; e0 += Ech) {
         const int ne = (int)std::min<long long>(Ech, E - e0);
         double *metric = (double *)workspace;
-        rc = hxg_metric_batched(space, p1, p2, p3, L, ne, kind + e0, params + 24 * e0,
+        rc = metric_run(space, p1, p2, p3, L, ne, kind + e0, params + 24 * e0,
                                 coef ? coef + e0 : nullptr, wgrid ? wgrid + e0 * L * L * L : nullptr,
                                 tables, metric, status + e0, stream);
         if (rc != HXG_OK) return rc;
@@ -616,18 +636,10 @@ int hxg_metric_batched(int space, int p1, int p2, int p3, int L, int E, const in
                        const double *params, const double *coef, const double *wgrid,
                        const double *tables, double *metric, int *status, void *stream)
 {
-    int rc = check_common(space, GENERAL, p1, p2, p3, L, E);
-    if (rc != HXG_OK) return rc;
-    if (E == 0) return HXG_OK;
-    if (!kind || !params || !tables || !metric || !status) return HXG_ERR_ARG;
-    SpacePlan P;
-    rc = build_plan(space, p1, p2, p3, P);
-    if (rc != HXG_OK) return rc;
-    const long long npts = (long long)E * L * L * L;
-    const int mgrid = (int)std::min<long long>((npts + 255) / 256, 148LL * 64);
-    metric_kernel<<<mgrid, 256, 0, (cudaStream_t)stream>>>(space, L, E, kind, params, coef, wgrid,
-                                                         tables, metric, status, P.nfields);
-    return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
+    // exported entry: the status word is written by the call (zeroed, then ORed)
+    if (E > 0 && status && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, (cudaStream_t)stream) != cudaSuccess)
+        return HXG_ERR_CUDA;
+    return metric_run(space, p1, p2, p3, L, E, kind, params, coef, wgrid, tables, metric, status, stream);
 }
 
 int hxg_contract_batched(int space, int p1, int p2, int p3, int L, int E, const double *tables,
@@ -707,7 +719,7 @@ int hxg_expand_full(int N, int E, const double *packed, double *full, void *stre
     if (N < 1 || E < 0 || !packed || !full) return HXG_ERR_ARG;
     const long long total = (long long)E * N * N;
     if (total == 0) return HXG_OK;
-    const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+    const int grid = (int)std::min<long long>((total + 255) / 256, (long long)sm_count() * 32);
     expand_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(N, total, packed, full);
     return cudaGetLastError() == cudaSuccess ? HXG_OK : HXG_ERR_CUDA;
 }
@@ -723,8 +735,8 @@ struct HostCtx {
     bool init = false;
     cudaStream_t s[2] = {nullptr, nullptr};
     cudaEvent_t inputs_ready = nullptr;
-    void *buf[9] = {nullptr};
-    size_t cap[9] = {0};
+    void *buf[11] = {nullptr};
+    size_t cap[11] = {0};
     void *get(int k, size_t bytes, bool &ok)
     {
         if (bytes == 0) return nullptr;
@@ -742,16 +754,21 @@ HostCtx g_host_ctx[64];
 }  // namespace
 
 int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, int E,
-                          const int *kind, const double *params, const double *coef, double *out,
-                          int *status)
+                          const double *nodes, const double *weights, const int *kind,
+                          const double *params, const double *coef, const double *wgrid,
+                          double *out, int *status)
 {
     int rc = check_common(space, path, p1, p2, p3, L, E);
     if (rc != HXG_OK) return rc;
     if (E == 0) return HXG_OK;
     if (!kind || !params || !out) return HXG_ERR_ARG;
+    if ((nodes == nullptr) != (weights == nullptr)) return HXG_ERR_ARG;
+    if (wgrid && path != GENERAL) return HXG_ERR_ARG;  // gram.py:93-98: constant weights only
     SpacePlan P;
     rc = build_plan(space, p1, p2, p3, P);
     if (rc != HXG_OK) return rc;
+    const int Lt = path == AFFINE ? 1 : L;  // the affine kernels read only the F tables
+    const bool user_rule = nodes && path != AFFINE;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return HXG_ERR_CUDA;
     HostCtx &cx = g_host_ctx[dev];
@@ -767,6 +784,7 @@ int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, in
     }
     const long long Pk = (long long)P.N * (P.N + 1) / 2;
     const size_t out_bytes_el = (size_t)Pk * sizeof(double);
+    const size_t L3 = (size_t)L * L * L;
     long long chunk_bytes = 64ll << 20;  // D2H granularity: small chunks overlap the copy engine sooner
     if (const char *c = getenv("HXG_HOST_CHUNK_MB")) chunk_bytes = std::max(1ll, atoll(c)) << 20;  // tuning
     long long ch = std::max<long long>(1, chunk_bytes / (long long)out_bytes_el);
@@ -780,12 +798,19 @@ int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, in
     double *d_out[2] = {(double *)cx.get(5, out_bytes_el * (size_t)ch, ok),
                         (double *)cx.get(6, out_bytes_el * (size_t)ch, ok)};
     void *d_ws[2] = {cx.get(7, ws, ok), cx.get(8, ws, ok)};
+    double *d_wgrid = wgrid ? (double *)cx.get(9, sizeof(double) * L3 * (size_t)E, ok) : nullptr;
+    double *d_rule = user_rule ? (double *)cx.get(10, sizeof(double) * 2 * (size_t)L, ok) : nullptr;
     if (!ok) return HXG_ERR_CUDA;
     cudaStream_t *s = cx.s;
     chk(cudaMemcpyAsync(d_kind, kind, sizeof(int) * (size_t)E, cudaMemcpyHostToDevice, s[0]));
     chk(cudaMemcpyAsync(d_params, params, sizeof(double) * 24 * (size_t)E, cudaMemcpyHostToDevice, s[0]));
     if (coef) chk(cudaMemcpyAsync(d_coef, coef, sizeof(double) * (size_t)E, cudaMemcpyHostToDevice, s[0]));
-    rc = hxg_make_tables(path == AFFINE ? 1 : L, nullptr, nullptr, d_tab, s[0]);
+    if (wgrid) chk(cudaMemcpyAsync(d_wgrid, wgrid, sizeof(double) * L3 * (size_t)E, cudaMemcpyHostToDevice, s[0]));
+    if (user_rule) {
+        chk(cudaMemcpyAsync(d_rule, nodes, sizeof(double) * (size_t)L, cudaMemcpyHostToDevice, s[0]));
+        chk(cudaMemcpyAsync(d_rule + L, weights, sizeof(double) * (size_t)L, cudaMemcpyHostToDevice, s[0]));
+    }
+    rc = hxg_make_tables(Lt, user_rule ? d_rule : nullptr, user_rule ? d_rule + L : nullptr, d_tab, s[0]);
     chk(cudaEventRecord(cx.inputs_ready, s[0]));
     chk(cudaStreamWaitEvent(s[1], cx.inputs_ready, 0));
     int i = 0;
@@ -793,18 +818,32 @@ int hxg_gram_batched_host(int space, int path, int p1, int p2, int p3, int L, in
         const int ne = (int)std::min<long long>(ch, E - e0);
         cudaStream_t st = s[i & 1];
         rc = hxg_gram_batched(space, path, p1, p2, p3, L, ne, d_kind + e0, d_params + 24 * e0,
-                              d_coef ? d_coef + e0 : nullptr, nullptr, d_tab, d_out[i & 1],
-                              d_status + e0, d_ws[i & 1], ws, st);
+                              d_coef ? d_coef + e0 : nullptr, d_wgrid ? d_wgrid + (size_t)e0 * L3 : nullptr,
+                              d_tab, d_out[i & 1], d_status + e0, d_ws[i & 1], ws, st);
         if (rc != HXG_OK) break;
         chk(cudaMemcpyAsync(out + e0 * Pk, d_out[i & 1], out_bytes_el * (size_t)ne,
                             cudaMemcpyDeviceToHost, st));
     }
     chk(cudaStreamSynchronize(s[0]));
     chk(cudaStreamSynchronize(s[1]));
-    if (status && ok && rc == HXG_OK)
-        chk(cudaMemcpy(status, d_status, sizeof(int) * (size_t)E, cudaMemcpyDeviceToHost));
     if (rc != HXG_OK) return rc;
-    return ok ? HXG_OK : HXG_ERR_CUDA;
+    if (!ok) return HXG_ERR_CUDA;
+    // the reference raises before returning any matrix (geometry.py:214-223,
+    // gram.py:170-174): flagged elements turn into an error code, with or without
+    // a status array to say which
+    std::vector<int> hs;
+    int *st_host = status;
+    if (!st_host) {
+        hs.resize((size_t)E);
+        st_host = hs.data();
+    }
+    if (cudaMemcpy(st_host, d_status, sizeof(int) * (size_t)E, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return HXG_ERR_CUDA;
+    int any = 0;
+    for (int e = 0; e < E; ++e) any |= st_host[e];
+    if (any & 2) return HXG_ERR_KIND;
+    if (any & 1) return HXG_ERR_DEGENERATE;
+    return HXG_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,25 @@
+// hxg_device.h -- host-side device queries shared by every launcher.
+//
+// Grid heuristics size persistent grids as a multiple of the SM count of the
+// CURRENT device (148 on B200) instead of a hard-coded constant.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+
+namespace hxg {
+
+// Number of SMs of the current device (cached per device ordinal; thread-safe).
+inline int sm_count()
+{
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v > 0) return v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev].store(v, std::memory_order_relaxed);
+    return v;
+}
+
+}  // namespace hxg

@@ -28,6 +28,7 @@
 #include "../../include/hexgram_b200.h"
 #include "hxg_geom.cuh"
 #include "hxg_plan.h"
+#include "hxg_device.h"
 
 using namespace hxg;
 
@@ -631,7 +632,7 @@ size_t ac_smem_bytes(int p0, int pr, int L, int c3)
 
 int grid_for(long long work, int threads)
 {
-    return (int)std::max<long long>(1, std::min<long long>((work + threads - 1) / threads, 148LL * 16));
+    return (int)std::max<long long>(1, std::min<long long>((work + threads - 1) / threads, (long long)sm_count() * 16));
 }
 
 }  // namespace

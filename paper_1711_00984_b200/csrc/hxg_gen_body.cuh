@@ -1,0 +1,151 @@
+// hxg_gen_body.cuh -- launchers of the compile-time specialized kernels of one
+// space S (isotropic orders p = 1..10, general path with L = p + 1, the
+// constant-Jacobian path and the extrusion path).  Each hxg_gen_<space>.cu
+// instantiates this body for its space so the four spaces compile in parallel.
+#pragma once
+#include <algorithm>
+#include <cstdlib>
+
+#include "hxg_affine_v2.cuh"
+#include "hxg_device.h"
+#include "hxg_extrusion.cuh"
+#include "hxg_general_v2.cuh"
+#include "hxg_general_v3.cuh"
+#include "hxg_v2_launch.h"
+
+namespace hxg {
+
+inline bool env_on(const char *name)
+{
+    const char *v = getenv(name);
+    return v && v[0] == '1';
+}
+
+// general_v3_kernel<H1, 7, 8> gave wrong results in round 1 under ptxas -O3
+// (DESIGN.md "Known compiler issue"); it runs only when HXG_V3_P7=1 asks for it
+// (the investigation harness, tools/v3p7_check.sh) -- otherwise H1 p = 7 takes v2.
+template <int S, int P>
+constexpr bool v3_default()
+{
+    return !(S == H1 && P == 7);
+}
+
+template <int S, int P>
+int gen_launch_one(const V2Args &a, cudaStream_t st)
+{
+    using C3 = V3Cfg<S, P, P + 1>;
+    if constexpr (C3::OK) {
+        // fused kernels (p <= 3) evaluate the geometry themselves: they take the
+        // fused call (metric == NULL); a call with a metric array runs v2
+        const bool want_v3 = v3_default<S, P>() || env_on("HXG_V3_P7");
+        if (want_v3 && !env_on("HXG_FORCE_V2") && (C3::FUSED == (a.metric == nullptr))) {
+            auto k3 = general_v3_kernel<S, P, P + 1>;
+            if (cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM_BYTES) != cudaSuccess)
+                return -5;
+            V3Args b;
+            b.tables = a.tables;
+            b.metric = a.metric;
+            b.out = a.out;
+            b.P = a.P;
+            b.E = a.E;
+            b.kind = a.kind;
+            b.params = a.params;
+            b.coef = a.coef;
+            b.wgrid = a.wgrid;
+            b.status = a.status;
+            // one element per item once the batch fills a wave of CTAs: the warps then
+            // flow from element to element (general_v3_kernel, HXG_V3_FLOW)
+            const int sms = sm_count();
+            const int want = sms * C3::MINB * 2;
+            b.split = a.E >= sms * C3::MINB ? 1 : (want + a.E - 1) / a.E;
+            if (b.split > 16) b.split = 16;
+            if (getenv("HXG_V3_SPLIT")) b.split = atoi(getenv("HXG_V3_SPLIT"));
+            // persistent CTAs (grid-stride over (element, part) items)
+            const long long items = (long long)a.E * b.split;
+            const int grid = (int)std::min<long long>(items, (long long)sms * C3::MINB * 2);
+            k3<<<grid, V3_THREADS, C3::SMEM_BYTES, st>>>(b);
+            return cudaGetLastError() == cudaSuccess ? 0 : -5;
+        }
+    }
+    using C = V2Cfg<S, P, P + 1>;
+    auto k = general_v2_kernel<S, P, P + 1>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
+        return -5;
+    const long long grid = (long long)a.E * C::NU;
+    if (grid >= (1ll << 31)) return -6;
+    k<<<(int)grid, V2_THREADS, C::SMEM_BYTES, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// returns 1 if no specialization exists for p, else 0 / negative error
+template <int S>
+int gen_launch(int p, const V2Args &a, cudaStream_t st)
+{
+    switch (p) {
+#define HXG_CASE(PP) case PP: return gen_launch_one<S, PP>(a, st);
+        HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
+        HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#undef HXG_CASE
+    }
+    return 1;
+}
+
+template <int S, int P>
+int aff_launch_one(const AffV2Args &a, cudaStream_t st)
+{
+    using C = AffCfg<S, P>;
+    if constexpr (C::SMEM_BYTES > 200 * 1024) {
+        return 1;  // row images do not fit: runtime-generic affine kernel
+    } else {
+        auto k = affine_v2_kernel<S, P>;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
+            return -5;
+        // low orders with many elements: one CTA per element (row groups are tiny);
+        // otherwise one CTA per packed row group
+        AffV2Args b = a;
+        b.rg = aff_row_groups(C::NU, a.P, a.E);
+        const long long grid = (long long)a.E * ((C::NU + b.rg - 1) / b.rg);
+        if (grid >= (1ll << 31)) return -6;
+        k<<<(int)grid, AFF2_THREADS, C::SMEM_BYTES, st>>>(b);
+        return cudaGetLastError() == cudaSuccess ? 0 : -5;
+    }
+}
+
+// specialized constant-Jacobian kernel; returns 1 if none exists for p
+template <int S>
+int aff_launch(int p, const AffV2Args &a, cudaStream_t st)
+{
+    switch (p) {
+#define HXG_CASE(PP) case PP: return aff_launch_one<S, PP>(a, st);
+        HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
+        HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#undef HXG_CASE
+    }
+    return 1;
+}
+
+// specialized extrusion-map kernel (simp_*_ext); returns 1 if none exists for p
+template <int S>
+int ext_launch(int p, const ExtArgs &a, cudaStream_t st)
+{
+    switch (p) {
+#define HXG_CASE(PP) case PP: return launch_ext_t<S, PP>(a, st);
+        HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
+        HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#undef HXG_CASE
+    }
+    return 1;
+}
+
+}  // namespace hxg
+
+// one translation unit per space: HXG_GEN_SPACE is the space code, HXG_GEN_NAME the
+// suffix of the launcher names declared in hxg_v2_launch.h
+#define HXG_GEN_CAT2(a, b) a##b
+#define HXG_GEN_CAT(a, b) HXG_GEN_CAT2(a, b)
+#define HXG_GEN_DEFINE_LAUNCHERS(SPACE, NAME)                                                             \
+    namespace hxg {                                                                                     \
+    int HXG_GEN_CAT(launch_v2_, NAME)(int p, const V2Args &a, cudaStream_t st) { return gen_launch<SPACE>(p, a, st); } \
+    int HXG_GEN_CAT(launch_aff_, NAME)(int p, const AffV2Args &a, cudaStream_t st) { return aff_launch<SPACE>(p, a, st); } \
+    int HXG_GEN_CAT(launch_ext_, NAME)(int p, const ExtArgs &a, cudaStream_t st) { return ext_launch<SPACE>(p, a, st); } \
+    }

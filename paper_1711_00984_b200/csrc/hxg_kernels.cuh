@@ -54,16 +54,28 @@ struct AffArgs {
 // ---------------------------------------------------------------------------
 // 1D tables
 // ---------------------------------------------------------------------------
+// The 1D tables follow the reference's arithmetic operation for operation, with
+// every product / sum rounded separately (no FMA contraction: numba compiles the
+// reference without fast-math), so the device rule and shape tables equal the
+// reference arrays to the last bit up to the cos() of the Newton start.
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rn_div(double a, double b) { return __ddiv_rn(a, b); }
+
+// P_L(x), P_L'(x) (quadrature.py:37-44): p = ((2k-1) x p - (k-1) p_prev) / k,
+// dp = L (x p - p_prev) / (x x - 1)
 __device__ inline void dev_legendre_pl(int L, double x, double &p, double &dp)
 {
     double pm = 1.0, pc = x;
     for (int k = 2; k <= L; ++k) {
-        const double pn = ((2 * k - 1) * x * pc - (k - 1) * pm) / k;
+        const double pn = rn_div(rn_sub(rn_mul(rn_mul((double)(2 * k - 1), x), pc), rn_mul((double)(k - 1), pm)),
+                                 (double)k);
         pm = pc;
         pc = pn;
     }
     p = pc;
-    dp = L * (x * pc - pm) / (x * x - 1.0);
+    dp = rn_div(rn_mul((double)L, rn_sub(rn_mul(x, pc), pm)), rn_sub(rn_mul(x, x), 1.0));
 }
 
 __device__ inline double dev_f00(int i, int j)
@@ -104,51 +116,64 @@ __global__ void tables_kernel(int L, const double *__restrict__ user_nodes,
 {
     __shared__ double s_nodes[LT];
     const int tid = threadIdx.x;
-    if (tid < LT) {
+    if (tid < 32) {  // one warp: L <= LT = 16 nodes
+        const bool act = tid < L;
         double node = 0.0, wt = 0.0;
-        if (tid < L) {
-            if (user_nodes) {
+        if (user_nodes) {
+            if (act) {
                 node = user_nodes[tid];
                 wt = user_wts[tid];
-            } else if (L == 1) {
+            }
+        } else if (L == 1) {
+            if (act) {
                 node = 0.5;
                 wt = 1.0;
-            } else {
-                // Newton on P_L from cos(pi (k - 1/4) / (L + 1/2)), k = L - tid so that
-                // the mapped nodes increase with tid (quadrature.py:53-65)
-                const int k = L - tid;
-                double x = cos(M_PI * (k - 0.25) / (L + 0.5));
-                for (int it = 0; it < 100; ++it) {
-                    double p, dp;
-                    dev_legendre_pl(L, x, p, dp);
-                    const double dx = p / dp;
-                    x -= dx;
-                    if (fabs(dx) < 1e-15) break;
-                }
-                double p, dp;
-                dev_legendre_pl(L, x, p, dp);
-                node = 0.5 * (1.0 + x);
-                wt = 0.5 * (2.0 / ((1.0 - x * x) * dp * dp));
+            }
+        } else {
+            // quadrature.py:53-65: x_k = cos(pi (k - 1/4) / (L + 1/2)), k = 1..L, all nodes
+            // updated together until max |dx| < 1e-15; lane tid holds k = L - tid so the
+            // mapped nodes increase with tid (nodes = 0.5 (1 + x[::-1]))
+            const int k = L - tid;
+            double x = act ? cos(rn_div(rn_mul(M_PI, rn_sub((double)k, 0.25)), rn_add((double)L, 0.5))) : 0.0;
+            for (int it = 0; it < 100; ++it) {
+                double p = 0.0, dp = 1.0;
+                if (act) dev_legendre_pl(L, x, p, dp);
+                const double dx = act ? rn_div(p, dp) : 0.0;
+                x = rn_sub(x, dx);
+                double m = fabs(dx);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+                if (m < 1e-15) break;
+            }
+            double p = 0.0, dp = 1.0;
+            if (act) dev_legendre_pl(L, x, p, dp);
+            if (act) {
+                const double w = rn_div(2.0, rn_mul(rn_mul(rn_sub(1.0, rn_mul(x, x)), dp), dp));
+                node = rn_mul(0.5, rn_add(1.0, x));
+                wt = rn_mul(0.5, w);
             }
         }
-        tab[TAB_NODES + tid] = node;
-        tab[TAB_WTS + tid] = wt;
-        s_nodes[tid] = node;
+        if (tid < LT) {
+            tab[TAB_NODES + tid] = node;
+            tab[TAB_WTS + tid] = wt;
+            s_nodes[tid] = node;
+        }
     }
     __syncthreads();
     // chi_k, chi'_k at each node (_kernels.py:29-43 with p = KT - 1)
     if (tid < LT) {
         const double xi = s_nodes[tid];
-        const double t = 2.0 * xi - 1.0;
+        const double t = rn_sub(rn_mul(2.0, xi), 1.0);
         double *chi = tab + TAB_T, *dchi = tab + TAB_T + KT * LT;
-        chi[0 * LT + tid] = 1.0 - xi;
+        chi[0 * LT + tid] = rn_sub(1.0, xi);
         chi[1 * LT + tid] = xi;
         dchi[0 * LT + tid] = -1.0;
         dchi[1 * LT + tid] = 1.0;
         double pm2 = 1.0, pm1 = t;
         for (int i = 2; i < KT; ++i) {
-            const double pi = ((2 * i - 1) * t * pm1 - (i - 1) * pm2) / i;
-            chi[i * LT + tid] = (pi - pm2) / (2.0 * (2 * i - 1));
+            const double pi = rn_div(rn_sub(rn_mul(rn_mul((double)(2 * i - 1), t), pm1), rn_mul((double)(i - 1), pm2)),
+                                     (double)i);
+            chi[i * LT + tid] = rn_div(rn_sub(pi, pm2), rn_mul(2.0, (double)(2 * i - 1)));
             dchi[i * LT + tid] = pm1;
             pm2 = pm1;
             pm1 = pi;

@@ -25,6 +25,8 @@ def _check(rc: int, what: str) -> None:
         raise InvalidOrderError(msg)
     if rc == _native.HXG_ERR_KIND:
         raise SimplificationNotApplicableError(msg)
+    if rc == _native.HXG_ERR_DEGENERATE:
+        raise DegenerateMapError(float("nan"), ())
     if rc in (_native.HXG_ERR_SPACE, _native.HXG_ERR_ARG):
         raise ValueError(msg)
     raise RuntimeError(msg)
@@ -61,11 +63,13 @@ class GramEngine:
         if nodes is None:
             rc = self.lib.hxg_make_tables(L, None, None, _ptr(t), ctypes.c_void_p(st.cuda_stream))
         else:
-            dn = torch.as_tensor(np.ascontiguousarray(nodes, dtype=np.float64)).to(self.device)
-            dw = torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float64)).to(self.device)
+            with torch.cuda.stream(st):
+                dn = torch.as_tensor(np.ascontiguousarray(nodes, dtype=np.float64)).to(self.device)
+                dw = torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float64)).to(self.device)
             rc = self.lib.hxg_make_tables(L, _ptr(dn), _ptr(dw), _ptr(t), ctypes.c_void_p(st.cuda_stream))
-            st.synchronize()
         _check(rc, "hxg_make_tables")
+        # the cached block is read later from any stream: complete it once here
+        st.synchronize()
         self._tables[key] = t
         return t
 
@@ -74,11 +78,14 @@ class GramEngine:
         so reuse on the same stream is safe and distinct streams never share one."""
         if nbytes == 0:
             return None
-        key = (stream or torch.cuda.current_stream(self.device)).cuda_stream
-        ws = self._ws.get(key)
+        st = stream or torch.cuda.current_stream(self.device)
+        ws = self._ws.get(st.cuda_stream)
         if ws is None or ws.numel() < nbytes:
-            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-            self._ws[key] = ws
+            # allocated on `st`: the caching allocator then recycles the block (and the
+            # one it replaces) only in `st` order
+            with torch.cuda.stream(st):
+                ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws[st.cuda_stream] = ws
         return ws
 
     # -- batched integration -------------------------------------------------
@@ -88,12 +95,21 @@ class GramEngine:
         """Integrate E elements.  kind/params/coef/wgrid are device tensors
         (int32 [E], float64 [E, 24], float64 [E], float64 [E, L^3]) or host
         arrays (copied in).  Returns (packed [E, N(N+1)/2] float64 device
-        tensor, status [E] int32 device tensor)."""
+        tensor, status [E] int32 device tensor).
+
+        The launch is ordered after the work already queued on the caller's
+        current stream (inputs produced there), whichever `stream` it runs on.
+        check_status=True waits for the call and raises DegenerateMapError /
+        SimplificationNotApplicableError from the device status word;
+        check_status=False returns without any host synchronisation (read the
+        status later with `raise_for_status(status, path, stream)`)."""
         dev = self.device
         p1, p2, p3 = (int(p) for p in orders)
         sc, pc = _native.SPACE_CODES[space], _native.PATH_CODES[path]
         N = self.lib.hxg_dim(sc, p1, p2, p3)
         _check(N if N < 0 else 0, "hxg_dim")
+        cur = torch.cuda.current_stream(dev)
+        st = stream or cur
         kind = torch.as_tensor(kind, dtype=torch.int32).to(dev).contiguous()
         E = int(kind.shape[0])
         params = torch.as_tensor(params, dtype=torch.float64).to(dev).reshape(E, 24).contiguous()
@@ -108,8 +124,14 @@ class GramEngine:
             out = torch.empty((E, P), dtype=torch.float64, device=dev)
         if status is None:
             status = torch.empty(E, dtype=torch.int32, device=dev)
-        st = stream or torch.cuda.current_stream(dev)
         tab = self.tables(L if path == "general" else max(L, 1), nodes, weights, st)
+        if st != cur:
+            # inputs (and a caller-provided `out`) were produced on the current stream;
+            # tensors allocated here on `cur` are used on `st` until it drains
+            st.wait_stream(cur)
+            for t in (kind, params, coef, wgrid, out, status):
+                if t is not None:
+                    t.record_stream(st)
         with self._lock:
             ws_bytes = self.lib.hxg_workspace_size(sc, pc, p1, p2, p3, L, E)
             ws = self.workspace(ws_bytes, st)
@@ -119,12 +141,16 @@ class GramEngine:
                                            ctypes.c_void_p(st.cuda_stream))
         _check(rc, "hxg_gram_batched")
         if check_status:
-            self.raise_for_status(status, path)
+            self.raise_for_status(status, path, st)
         return out, status
 
     @staticmethod
-    def raise_for_status(status: torch.Tensor, path: str) -> None:
-        s = status.cpu().numpy()
+    def raise_for_status(status: torch.Tensor, path: str, stream=None) -> None:
+        """Raise the reference's exception for the first flagged element.  The
+        status word is read on `stream` (the stream the call ran on)."""
+        st = stream or torch.cuda.current_stream(status.device)
+        with torch.cuda.stream(st):
+            s = status.cpu().numpy()
         bad = np.nonzero(s)[0]
         if bad.size == 0:
             return
@@ -144,18 +170,37 @@ class GramEngine:
 
     def integrate_host(self, space: str, path: str, orders, L: int, kind: np.ndarray,
                        params: np.ndarray, coef: np.ndarray | None, out: np.ndarray,
-                       status: np.ndarray | None = None) -> None:
-        """Host buffers in, host buffer out (hxg_gram_batched_host)."""
+                       status: np.ndarray | None = None, nodes=None, weights=None,
+                       wgrid: np.ndarray | None = None) -> None:
+        """Host buffers in, host buffer out (hxg_gram_batched_host): the
+        reference's kernel seam kern(p1, p2, p3, nodes, wts, kind, par, wgrid)
+        (gram.py:154-157) batched.  nodes/weights: a user Rule1D (None: Gauss
+        rule of L points); wgrid: sampled mass weights [E, L^3] (general path)."""
         p1, p2, p3 = (int(p) for p in orders)
         kind = np.ascontiguousarray(kind, dtype=np.int32)
         params = np.ascontiguousarray(params, dtype=np.float64)
         coef = None if coef is None else np.ascontiguousarray(coef, dtype=np.float64)
+        if nodes is not None:
+            nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+            weights = np.ascontiguousarray(weights, dtype=np.float64)
+            if nodes.size != L or weights.size != L:
+                raise ValueError("nodes / weights must hold L points")
         E = kind.shape[0]
+        if wgrid is not None:
+            wgrid = np.ascontiguousarray(wgrid, dtype=np.float64)
+            if wgrid.size != E * L ** 3:
+                raise ValueError("wgrid must hold L^3 nodes per element")
         rc = self.lib.hxg_gram_batched_host(
             _native.SPACE_CODES[space], _native.PATH_CODES[path], p1, p2, p3, L, E,
+            None if nodes is None else nodes.ctypes.data,
+            None if weights is None else weights.ctypes.data,
             kind.ctypes.data, params.ctypes.data, None if coef is None else coef.ctypes.data,
+            None if wgrid is None else wgrid.ctypes.data,
             out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr(),
             None if status is None else status.ctypes.data)
+        if rc == _native.HXG_ERR_DEGENERATE and status is not None:
+            bad = np.nonzero(status & 1)[0]
+            raise DegenerateMapError(float("nan"), tuple(int(e) for e in bad[:1]))
         _check(rc, "hxg_gram_batched_host")
 
 

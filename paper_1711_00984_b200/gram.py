@@ -183,14 +183,44 @@ def gram_simplified(sig: SpaceSignature, emap: ElementMap, ftab: FTable | None =
     return GramResult(G, counters(sig.space, sig.orders, "simplified", L, klass="extrusion"))
 
 
+def _rule3d_factor(rule3d: Rule3D) -> Rule1D:
+    """The 1D factor of a tensor-product Rule3D (quadrature.py:69-83: points
+    lexicographic in (l, m, n), weights w_l w_m w_n).  The Gauss tensor rule of
+    its order returns gauss_rule(order) itself (bit-exact nodes/weights);
+    any other tensor rule its extracted factor; a rule that is not a tensor
+    product raises ValueError (the device kernels are sum-factorized)."""
+    pts = np.asarray(rule3d.points, dtype=np.float64)
+    wts = np.asarray(rule3d.weights, dtype=np.float64)
+    n3 = wts.size
+    L = int(round(n3 ** (1.0 / 3.0)))
+    if L < 1 or L ** 3 != n3 or pts.shape != (n3, 3):
+        raise ValueError("rule3d is not a tensor-product rule (L^3 points expected)")
+    g = gauss_rule(L)
+    nodes = pts[:L, 2].copy()
+    w0 = np.cbrt(wts[0])
+    weights = wts[:L] / (w0 * w0)
+    cand = g if (np.array_equal(nodes, g.nodes) and np.allclose(weights, g.weights, rtol=1e-14, atol=0)) \
+        else Rule1D(nodes=nodes, weights=weights, order=L)
+    ll, mm, nn = np.meshgrid(np.arange(L), np.arange(L), np.arange(L), indexing="ij")
+    tp = np.stack([cand.nodes[ll.ravel()], cand.nodes[mm.ravel()], cand.nodes[nn.ravel()]], axis=1)
+    tw = cand.weights[ll.ravel()] * cand.weights[mm.ravel()] * cand.weights[nn.ravel()]
+    if not (np.array_equal(tp, pts) and np.allclose(tw, wts, rtol=1e-13, atol=0)):
+        raise ValueError("rule3d is not a tensor-product rule; the device path integrates "
+                         "with sum factorization over a 1D rule")
+    return cand
+
+
 def gram_conventional(sig: SpaceSignature, emap: ElementMap, rule3d: Rule3D | None = None, *,
                       mass_weight=None) -> GramResult:
     """Conventional-backend signature (gram.py:101-124).  The O(p^9) algorithm
     is out of scope; the matrix is the same tensor-rule integral computed by
-    the sum-factorized device kernel with the rule's 1D factor, and the
-    counters are the conventional closed forms."""
-    L = rule3d.order if rule3d is not None else default_rule_order(sig.space, sig.orders)
-    rule = gauss_rule(L)
+    the sum-factorized device kernel with the rule's 1D factor
+    (`_rule3d_factor`), and the counters are the conventional closed forms."""
+    if rule3d is None:
+        rule = gauss_rule(default_rule_order(sig.space, sig.orders))
+    else:
+        rule = _rule3d_factor(rule3d)
+    L = rule.nodes.size
     wgrid = _weight_grid(emap, rule.nodes, mass_weight)
     G = _device_matrix(sig, emap, "general", L, _scalar(mass_weight), wgrid, rule)
     return GramResult(G, counters(sig.space, sig.orders, "conventional", L))
@@ -227,22 +257,29 @@ def gram_block(sig: SpaceSignature, emap: ElementMap, backend: str = "convention
 
 
 def gram_batched(space: str, orders, kind, params, coef=None, *, path: str = "general",
-                 rule_order: int | None = None, wgrid=None, out=None, stream=None, device=None):
+                 rule_order: int | None = None, wgrid=None, out=None, stream=None, device=None,
+                 rule: Rule1D | None = None, check_status: bool = True):
     """Batched native entry: E elements -> packed upper triangles.
 
     kind int32 [E], params float64 [E, 24], coef float64 [E] (mass-term
     weight, default 1), optional wgrid float64 [E, L^3]; torch tensors on the
     device or host arrays.  path: "general" (gram_tensorized), "affine"
     (constant-Jacobian gram_simplified) or "extrusion" (extrusion-map
-    gram_simplified, rule_order points in xi2 and xi3).  Returns (packed
+    gram_simplified, rule_order points in xi2 and xi3).  `rule` (a Rule1D)
+    replaces the Gauss rule of `rule_order` points.  Returns (packed
     [E, N(N+1)/2] float64 CUDA tensor, status [E] int32 CUDA tensor) --
-    row-major upper triangles."""
+    row-major upper triangles.  check_status=False skips the host read of the
+    status word (no synchronisation; see GramEngine.raise_for_status)."""
     from .engine import get_engine
 
     sig = SpaceSignature(space, orders)
     L = rule_order if rule_order is not None else default_rule_order(space, sig.orders)
+    nodes = weights = None
+    if rule is not None:
+        L = int(rule.nodes.size)
+        nodes, weights = rule.nodes, rule.weights
     if path == "affine":
-        L = 1
+        L, nodes, weights = 1, None, None
     eng = get_engine(device)
     return eng.integrate(space, path, sig.orders, L, kind, params, coef, wgrid, out=out,
-                         stream=stream)
+                         nodes=nodes, weights=weights, stream=stream, check_status=check_status)

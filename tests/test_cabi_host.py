@@ -84,3 +84,11 @@ def test_workspace_size_is_host_only(lib):
     big = lib.hxg_workspace_size(0, 0, 2, 2, 2, 3, 10 ** 8)
     assert 0 < big <= 512 * 2 ** 20  # chunked: bounded workspace
     assert lib.hxg_tables_doubles() > 0
+
+
+def test_table_layout_constants(lib):
+    """The Python mirror of the device table layout (used to read tables back)
+    matches the library's block size (hxg_plan.h)."""
+    from paper_1711_00984_b200 import _native as nat
+
+    assert lib.hxg_tables_doubles() == nat.TAB_TOTAL

@@ -120,3 +120,31 @@ def test_seeded_batches_are_valid_maps():
         for e in range(8):
             kind = "trilinear" if b.kind[e] == 4 else "general-affine"
             hx.ElementMap(kind, b.params[e])  # orientation check passes
+
+
+def test_rule3d_factor():
+    """gram_conventional's Rule3D handling (gram.py:101-124): the Gauss tensor
+    rule maps back to gauss_rule(L) exactly, a non-Gauss tensor rule to its own
+    1D factor, and a rule that is not a tensor product is rejected."""
+    import numpy as np
+    import pytest
+
+    from paper_1711_00984_b200.gram import _rule3d_factor
+    from paper_1711_00984_b200.quadrature import Rule3D, gauss_rule, tensor_rule
+
+    for L in range(1, 12):
+        r, g = _rule3d_factor(tensor_rule(L)), gauss_rule(L)
+        np.testing.assert_array_equal(r.nodes, g.nodes)
+        np.testing.assert_array_equal(r.weights, g.weights)
+    n = np.array([0.1, 0.5, 0.8])
+    w = np.array([0.3, 0.3, 0.4])
+    pts = np.stack(np.meshgrid(n, n, n, indexing="ij"), -1).reshape(-1, 3)
+    wts = np.einsum("i,j,k->ijk", w, w, w).ravel()
+    r = _rule3d_factor(Rule3D(pts, wts, 3))
+    np.testing.assert_array_equal(r.nodes, n)
+    np.testing.assert_allclose(r.weights, w, rtol=1e-15)
+    bad = pts.copy()
+    bad[5, 0] = 0.33
+    for P, W in ((bad, wts), (pts, wts * np.linspace(1, 1.1, 27)), (pts[:20], wts[:20])):
+        with pytest.raises(ValueError):
+            _rule3d_factor(Rule3D(P, W, 3))
