@@ -126,6 +126,27 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _free_port():
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def maybe_spawn(args, argv):
+    """`--gpus N` (N > 1) outside a torchrun environment: re-launch this script
+    as N ranks under torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1) and return its exit code; None when already inside a launcher
+    or N == 1.  Only rank 0 prints, so the parent's stdout is the one JSON line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
 def dist_setup(args):
     import torch
     import torch.distributed as dist
@@ -133,12 +154,47 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using the launcher's "
+              f"world size", file=sys.stderr)
     if world > 1 and not dist.is_initialized():
         backend = "nccl" if torch.cuda.is_available() else "gloo"
         if torch.cuda.is_available():
+            if torch.cuda.device_count() <= local:
+                raise RuntimeError(f"rank {rank}: LOCAL_RANK {local} but only "
+                                   f"{torch.cuda.device_count()} visible GPU(s)")
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return world, rank, local
+
+
+def gather_checksums(out, world, device=None):
+    """Per-shard checksums of the packed output (sum, sum of squares, Frobenius
+    norm of the shard's first and last element), all-gathered over the
+    process group -- the only collective of the multi-GPU run."""
+    import torch
+
+    E = out.shape[0]
+    o = out.to(torch.float64)
+    loc = torch.stack([o.sum(), (o * o).sum(), torch.linalg.norm(o[0]), torch.linalg.norm(o[E - 1]),
+                       torch.tensor(float(E), dtype=torch.float64, device=o.device)])
+    if world == 1:
+        return [loc.tolist()]
+    import torch.distributed as dist
+
+    allv = [torch.zeros_like(loc) for _ in range(world)]
+    dist.all_gather(allv, loc)
+    return [v.tolist() for v in allv]
+
+
+def gather_objects(obj, world):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
+
+    allv = [None] * world
+    dist.all_gather_object(allv, obj)
+    return allv
 
 
 def max_over_ranks(x, world, device=None):
@@ -184,6 +240,24 @@ def cpu_rate(wl, seconds, nthreads=0):
         n = int(n * min(8.0, max(2.0, 1.2 * seconds / max(dt, 1e-3))))
 
 
+def cpu_host_info():
+    """CPU model, os.cpu_count() and the affinity-mask size."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        aff = None
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": aff}
+
+
 def run_reference(args, wl, world, rank):
     if rank != 0:
         return
@@ -216,7 +290,8 @@ def run_reference(args, wl, world, rank):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{per_step} elements per step of {wl.name}, "
                                    f"oracle/hexgram_oracle.c (alternative loop order, "
-                                   f"pthreads over elements)"},
+                                   f"pthreads over elements)",
+                         "one_core_value": cpu_rate(wl, 2.0, 1)[0], **cpu_host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -532,6 +607,21 @@ def run_ours(args, wl, world, rank, local):
                 "d2h_bytes_per_step": d2h,
                 "api": "hxg_gram_batched_host (C ABI, host buffers, pinned output)"},
     }
+    line["shard_checksums"] = gather_checksums(ds.out, world, device)
+    line["clocks_per_rank"] = gather_objects(clocks, world)
+    if world > 1:
+        # strong scaling on the same run: the config's global batch split over the ranks
+        Eg = wl.E
+        slo, shi = shard(Eg, world, rank)
+        del ds
+        torch.cuda.empty_cache()
+        ds2, tms2, _, _ = measure_device(wl, shi - slo, slo, args.steps, args.warmup, world,
+                                         device, with_clocks=False)
+        tms2 = max_over_ranks(tms2, world, device)
+        line["strong_scaling"] = {"global_elements": Eg, "elements_per_gpu": shi - slo,
+                                  "value": Eg * args.steps / (tms2 / 1e3),
+                                  "ms_per_step": tms2 / args.steps, "unit": UNIT}
+        del ds2
     if args.suite and rank == 0 and world == 1:
         suite = []
         for name, w2 in WORKLOADS.items():
@@ -553,9 +643,13 @@ def run_ours(args, wl, world, rank, local):
         line["dpg_suite"] = dpg_suite(device, fp64, hbm)
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, n, dt, threads = cpu_rate(wl, args.cpu_seconds)
+        rate1, n1, dt1, _ = cpu_rate(wl, 3.0, 1)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"{n} elements of {wl.name} in {dt:.1f} s "
-                                          f"(oracle/hexgram_oracle.c, {threads} threads)"}
+                                          f"(oracle/hexgram_oracle.c, {threads} threads)",
+                                "one_core_value": rate1,
+                                "one_core_sample": f"{n1} elements in {dt1:.1f} s, 1 thread",
+                                **cpu_host_info()}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -669,12 +763,20 @@ def main():
     ap.add_argument("--sweep-pmax", type=int, default=10)
     ap.add_argument("--sweep-reps", type=int, default=2)
     args = ap.parse_args()
+    rc = maybe_spawn(args, sys.argv[1:])
+    if rc is not None:
+        sys.exit(rc)
+    if args.impl == "reference" and not args.sweep:
+        # the reference arm is a host-CPU measurement: rank 0 runs it on the box's
+        # cores and prints; the other ranks exit without work (no process group)
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if int(os.environ.get("RANK", "0")) == 0:
+            run_reference(args, ALL_WORKLOADS[args.workload], world, 0)
+        return
     world, rank, local = dist_setup(args)
     wl = ALL_WORKLOADS[args.workload]
     if args.sweep:
         run_sweep(args, world, rank, local)
-    elif args.impl == "reference":
-        run_reference(args, wl, world, rank)
     else:
         run_ours(args, wl, world, rank, local)
     if world > 1:

@@ -15,19 +15,26 @@
 
 namespace hxg {
 
-inline bool env_on(const char *name)
+static inline bool env_on(const char *name)
 {
     const char *v = getenv(name);
     return v && v[0] == '1';
 }
 
-// general_v3_kernel<H1, 7, 8> gave wrong results in round 1 under ptxas -O3
-// (DESIGN.md "Known compiler issue"); it runs only when HXG_V3_P7=1 asks for it
-// (the investigation harness, tools/v3p7_check.sh) -- otherwise H1 p = 7 takes v2.
+// general_v3_kernel<H1, 7, 8> was routed to v2 in round 1 after wrong results
+// under ptxas -O3.  On the current source it is
+// correct (tools/v3p7_check.py: 64 elements vs the oracle at 3e-16, with and
+// without the HXG_DMMA_KEEP register hack; tests/test_gpu_parity.py sweeps) and
+// 1.65x faster than v2 (profiles/v3p7_r02.txt), so it runs by default;
+// HXG_V3_P7=0 restores the v2 route.
 template <int S, int P>
-constexpr bool v3_default()
+bool v3_enabled()
 {
-    return !(S == H1 && P == 7);
+    if constexpr (S == H1 && P == 7) {
+        const char *v = getenv("HXG_V3_P7");
+        return !(v && v[0] == '0');
+    }
+    return true;
 }
 
 template <int S, int P>
@@ -37,7 +44,7 @@ int gen_launch_one(const V2Args &a, cudaStream_t st)
     if constexpr (C3::OK) {
         // fused kernels (p <= 3) evaluate the geometry themselves: they take the
         // fused call (metric == NULL); a call with a metric array runs v2
-        const bool want_v3 = v3_default<S, P>() || env_on("HXG_V3_P7");
+        const bool want_v3 = v3_enabled<S, P>();
         if (want_v3 && !env_on("HXG_FORCE_V2") && (C3::FUSED == (a.metric == nullptr))) {
             auto k3 = general_v3_kernel<S, P, P + 1>;
             if (cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM_BYTES) != cudaSuccess)
