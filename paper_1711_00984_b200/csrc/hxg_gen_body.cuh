@@ -11,6 +11,7 @@
 #include "hxg_extrusion.cuh"
 #include "hxg_general_v2.cuh"
 #include "hxg_general_v3.cuh"
+#include "hxg_general_pw.cuh"
 #include "hxg_v2_launch.h"
 
 namespace hxg {
@@ -37,9 +38,41 @@ bool v3_enabled()
     return true;
 }
 
+// warp-owned P-form kernel (hxg_general_pw.cuh): default for p >= 8 (digit
+// extents 9-11, where the v3 8x8 tiles do not fit and v2's CTA-chunked stages
+// stall at barriers) in H1 and H(curl), and for H(div) at p = 8; measured
+// (profiles/pw_r02.txt) v2 stays ahead for H(div) p = 9, 10 and is kept for L2.
+// HXG_PW=1 selects it for every order it supports, HXG_PW=0 never.
+template <int S, int P>
+bool pw_enabled()
+{
+    const char *v = getenv("HXG_PW");
+    if (v && v[0] == '0') return false;
+    if (v && v[0] == '1') return true;
+    return P >= 8 && (S == H1 || S == HCURL || (S == HDIV && P == 8));
+}
+
 template <int S, int P>
 int gen_launch_one(const V2Args &a, cudaStream_t st)
 {
+    using CP = PWCfg<S, P, P + 1>;
+    if constexpr (CP::OK && P >= 4) {
+        if (a.metric != nullptr && pw_enabled<S, P>() && !env_on("HXG_FORCE_V2")) {
+            auto kp = general_pw_kernel<S, P, P + 1>;
+            if (cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::SMEM_BYTES) != cudaSuccess)
+                return -5;
+            PWArgs b;
+            b.tables = a.tables;
+            b.metric = a.metric;
+            b.out = a.out;
+            b.P = a.P;
+            b.E = a.E;
+            const long long items = (long long)a.E * CP::NU;
+            const int grid = (int)std::min<long long>(items, (long long)sm_count() * CP::MINB);
+            kp<<<grid, PW_THREADS, CP::SMEM_BYTES, st>>>(b);
+            return cudaGetLastError() == cudaSuccess ? 0 : -5;
+        }
+    }
     using C3 = V3Cfg<S, P, P + 1>;
     if constexpr (C3::OK) {
         // fused kernels (p <= 3) evaluate the geometry themselves: they take the
