@@ -49,7 +49,7 @@ bool pw_enabled()
     const char *v = getenv("HXG_PW");
     if (v && v[0] == '0') return false;
     if (v && v[0] == '1') return true;
-    return P >= 8 && (S == H1 || S == HCURL || (S == HDIV && P == 8));
+    return P >= 8 && S != L2;
 }
 
 template <int S, int P>
@@ -69,7 +69,7 @@ int gen_launch_one(const V2Args &a, cudaStream_t st)
             b.E = a.E;
             const long long items = (long long)a.E * CP::NU;
             const int grid = (int)std::min<long long>(items, (long long)sm_count() * CP::MINB);
-            kp<<<grid, PW_THREADS, CP::SMEM_BYTES, st>>>(b);
+            kp<<<grid, CP::THREADS, CP::SMEM_BYTES, st>>>(b);
             return cudaGetLastError() == cudaSuccess ? 0 : -5;
         }
     }

@@ -50,11 +50,23 @@ namespace hxg {
 #define HXG_PW_WO -1
 #endif
 __host__ __device__ constexpr bool pw_direct(int S) { return HXG_PW_WO < 0 ? (S == H1 || S == HCURL) : HXG_PW_WO == 1; }
+// test digits i3 per work unit (stage-C rows (kk, i2) with kk < K; each packed row
+// segment is K * n1a * n2a long, so the bulk write-out issues K times fewer copies
+// per byte); default 1, HXG_PW_K_HDIV / HXG_PW_K_L2 for the staged spaces
+#ifndef HXG_PW_K_HDIV
+#define HXG_PW_K_HDIV 1
+#endif
+#ifndef HXG_PW_K_L2
+#define HXG_PW_K_L2 1
+#endif
 #ifndef HXG_PW_STCS
 #define HXG_PW_STCS 1  // direct write-out with evict-first streaming stores (else write-back)
 #endif
 #ifndef HXG_PW_CTW_NK
 #define HXG_PW_CTW_NK 6  // two column tiles per step when the pair has <= this many k-steps
+#endif
+#ifndef HXG_PW_SKIP_WO
+#define HXG_PW_SKIP_WO 0  // timing experiment only (wrong results): 1 no copy-out, 2 no staging either
 #endif
 constexpr int PW_WARPS = HXG_PW_WARPS;
 constexpr int PW_THREADS = PW_WARPS * 32;
@@ -78,7 +90,12 @@ struct PWCfg {
     }
     static constexpr int NT = maxt();
     __host__ __device__ static constexpr int nk(int a, int b) { return (make_pair_plan(S, a, b).nh * L + 3) / 4; }
-    __host__ __device__ static constexpr int ctw(int a, int b) { return nk(a, b) <= HXG_PW_CTW_NK ? 2 : 1; }
+    // two column tiles per step only with the direct write-out: the staged spaces keep
+    // one (fewer staging slots; measured faster at p = 9, 10)
+    __host__ __device__ static constexpr int ctw(int a, int b)
+    {
+        return (pw_direct(S) && nk(a, b) <= HXG_PW_CTW_NK) ? 2 : 1;
+    }
     __host__ __device__ static constexpr int maxnk()
     {
         int m = 1;
@@ -87,7 +104,9 @@ struct PWCfg {
         return m;
     }
     static constexpr int NKS = maxnk();
-    static constexpr int N2M = C2::N2;
+    static constexpr int K = S == HDIV ? HXG_PW_K_HDIV : (S == L2 ? HXG_PW_K_L2 : 1);
+    __host__ __device__ static constexpr int kcnt(int r) { return (r + K - 1) / K; }  // units over r digits i3
+    static constexpr int N2M = K * C2::N2;  // stage-C rows (kk, i2) per trial digit j2
     // most trial digits j1 beyond the first that one step (CTW 8-column tiles of
     // (j1, i1)) touches
     __host__ __device__ static constexpr int jspan()
@@ -105,19 +124,22 @@ struct PWCfg {
     // writes plus one whose bulk copies may still be reading
     static constexpr int NSLOT = JSPAN + 2;
     static constexpr int NSLOT_SMEM = pw_direct(S) ? 0 : NSLOT;
-    static constexpr int SEG = ((C12 + 2 + 1) / 2) * 2;  // staging segment stride (even, >= C12 + 1)
+    static constexpr int WARPS = PW_WARPS, THREADS = PW_THREADS;
+    static constexpr int SEG = ((K * C12 + 2 + 1) / 2) * 2;  // staging segment stride (even, >= K C12 + 1)
     // per-warp shared memory (doubles) for groups of at most rj in {1, 2, 4, 8} trial digits
-    __host__ __device__ static constexpr int rtmax(int rj) { return (rj * N2M + 7) / 8; }
+    __host__ __device__ static constexpr int rtmax(int rj) { return K * ((rj * C2::N2 + 7) / 8); }
     __host__ __device__ static constexpr int w_tot(int rj)
     {
-        return NT * LP + NG * LT * LQ * 32 + rtmax(rj) * NKS * 32 + NSLOT_SMEM * rj * SEG;
+        return K * NT * LP + K * NG * LT * LQ * 32 + rtmax(rj) * NKS * 32 + NSLOT_SMEM * rj * SEG;
     }
-    __host__ __device__ static constexpr int cta_bytes(int rj) { return (2 * KT * LP + PW_WARPS * w_tot(rj)) * 8 + 16; }
-    // H1 groups stay at <= 4 trial digits: general_pw_kernel<H1, 7, 8> with one 8-digit
-    // group is wrong under ptxas -O1 / -O3 and bit-exact at -O0 (CUDA 12.9; every
-    // other instantiation, 8-digit groups included, matches the oracle -- see
-    // profiles/pw_h1p7_r02.txt); the 4-digit grouping of the same kernel is exact
-    static constexpr int RJCAP = S == H1 ? 4 : 8;
+    __host__ __device__ static constexpr int cta_bytes(int rj) { return (2 * KT * LP + WARPS * w_tot(rj)) * 8 + 16; }
+    // RJCAP: optional cap on the trial digits per group (test hook; the round-2 H1 p = 7
+    // failure of 8-digit groups was a missing warp reconvergence before mma.sync, fixed
+    // by the __syncwarp() ahead of every DMMA block -- profiles/pw_h1p7_r02.txt)
+#ifndef HXG_PW_RJCAP_H1
+#define HXG_PW_RJCAP_H1 8
+#endif
+    static constexpr int RJCAP = S == H1 ? HXG_PW_RJCAP_H1 : 8;
     __host__ __device__ static constexpr int pick_rj()
     {
         int r = 1;
@@ -128,8 +150,8 @@ struct PWCfg {
     static constexpr int RJ = pick_rj();
     static constexpr int RTM = rtmax(RJ);
     static constexpr int W_P = 0;                        // [NT][LP] stage-A 1D products
-    static constexpr int W_A = W_P + NT * LP;            // [NG][LT][LQ][32] Abar (stage-B B fragments)
-    static constexpr int W_B = W_A + NG * LT * LQ * 32;  // [RTM][NKS][32] B_h (stage-C A fragments)
+    static constexpr int W_A = W_P + K * NT * LP;            // [K][NG][LT][LQ][32] Abar (stage-B B fragments)
+    static constexpr int W_B = W_A + K * NG * LT * LQ * 32;  // [RTM][NKS][32] B_h (stage-C A fragments)
     static constexpr int W_S = W_B + RTM * NKS * 32;     // [NSLOT][RJ][SEG] staging
     static constexpr int W_TOT = w_tot(RJ);
     static constexpr int OFF_T = 0;
@@ -143,7 +165,12 @@ struct PWCfg {
     {
         int u = 0;
         for (int b = 0; b < NB; ++b)
-            for (int a = b; a < NB; ++a) u += a == b ? n(b, 2) * (n(b, 2) + 1) / 2 : n(b, 2) * n(a, 2);
+            for (int a = b; a < NB; ++a) {
+                if (a == b)
+                    for (int j3 = 0; j3 < n(b, 2); ++j3) u += kcnt(n(b, 2) - j3);
+                else
+                    u += n(b, 2) * kcnt(n(a, 2));
+            }
         return u;
     }
     static constexpr int NU = units();
@@ -157,6 +184,20 @@ struct PWArgs {
     int E;
 };
 
+// Row layout of a group of NJ2 trial digits: rows are kk-major blocks (one per test
+// digit kk < K of the unit) of RPK = NJ2 n2a rows rounded up to whole 8-row tiles, so
+// every row tile belongs to one kk (stage B's B operand, Abar_kk, is shared by the
+// tile's rows); inside a block, row r = i2 NJ2 + jj2.  off(rt) is the column offset
+// (kk n1a n2a + i2 n1a, relative to the lane's row in tile 0) of row tile rt.
+template <int NJ2, int K, int n1a, int n2a>
+struct PWRows {
+    static constexpr int RPK = ((NJ2 * n2a + 7) / 8) * 8;
+    static constexpr int TPK = RPK / 8;        // row tiles per test digit
+    static constexpr int NRT = K * TPK;
+    static constexpr int NROWK = NJ2 * n2a;    // rows of one digit block that exist
+    __host__ __device__ static constexpr int off(int rt) { return (rt / TPK) * n1a * n2a + (rt % TPK) * (8 / NJ2) * n1a; }
+};
+
 // Per-lane state of one group's stage C (see pw_group)
 struct PWLane {
     int rowoff0;  // staging offset of this lane's row in row tile 0 (jj2 SEG + i2 n1a)
@@ -165,6 +206,7 @@ struct PWLane {
     double *gbase;  // &G(row 0, column I0 + i2 n1a) of this lane's row in row tile 0, minus the row start
     int Jb;         // packed row of (j1 = 0, this lane's j2)
     int thr0;       // diagonal units: columns c < J - I0 of row J are below the diagonal (-1 << 30 otherwise)
+    int kc;         // test digits of the unit (row tiles of digits kk >= kc are not written)
 };
 
 // One stage-C step: CTW column tiles starting at column tile ct, all row tiles of the
@@ -177,9 +219,13 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
     constexpr int LP = C::LP, NKS = C::NKS, SEG = C::SEG, NSLOT = C::NSLOT, RJ = C::RJ;
     constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1), n1b = C::n(B, 0);
     constexpr int NCOL = n1b * n1a;
-    constexpr int NROW = NJ2 * n2a, NRT = (NROW + 7) / 8;
-    constexpr int RSTRIDE = (8 / NJ2) * n1a;  // staging stride between row tiles
+    using R = PWRows<NJ2, C::K, n1a, n2a>;
+    constexpr int NRT = R::NRT, TPK = R::TPK;
     const int lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
+    // mma.sync is .aligned: the whole warp must execute it converged, and the previous
+    // step ended in lane-divergent stores (independent thread scheduling does not
+    // promise reconvergence there)
+    __syncwarp();
     double Bp[CTW][NK];
 #pragma unroll
     for (int w = 0; w < CTW; ++w) {
@@ -203,7 +249,7 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
 #pragma unroll
             for (int w = 0; w < CTW; ++w) dmma_8x8x4(d[w][rt][0], d[w][rt][1], a, Bp[w][ks]);
         }
-    const bool lastv = (NRT - 1) * 8 + g8 < NROW;  // this lane's row of the last row tile exists
+    const bool lastv = (TPK - 1) * 8 + g8 < R::NROWK;  // this lane's row of a digit's last row tile exists
     if constexpr (pw_direct(S)) {
         constexpr int N = C::N;
 #pragma unroll
@@ -215,13 +261,13 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
                     const int j1 = oc / n1a, i1 = oc - (oc / n1a) * n1a;
                     const int J = ln.Jb + j1;
                     double *dst = ln.gbase + (J * N - J * (J + 1) / 2 + i1);
-                    // row-tile offsets rt * RSTRIDE below thr sit left of the diagonal
+                    // row-tile offsets below thr sit left of the diagonal
                     const int thr = ln.thr0 + j1 - i1;
 #pragma unroll
                     for (int rt = 0; rt < NRT; ++rt)
-                        if ((rt < NRT - 1 || lastv) && rt * RSTRIDE >= thr) {
-                            if constexpr (HXG_PW_STCS) __stcs(dst + rt * RSTRIDE, d[w][rt][c]);
-                            else dst[rt * RSTRIDE] = d[w][rt][c];
+                        if ((rt % TPK < TPK - 1 || lastv) && R::off(rt) >= thr && (C::K == 1 || rt / TPK < ln.kc)) {
+                            if constexpr (HXG_PW_STCS) __stcs(dst + R::off(rt), d[w][rt][c]);
+                            else dst[R::off(rt)] = d[w][rt][c];
                         }
                 }
             }
@@ -240,7 +286,7 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
                 double *base = sS + ((seq + j1) % NSLOT) * (RJ * SEG) + ln.rowoff0 + i1 + ((ln.pat >> (j1 & 3)) & 1);
 #pragma unroll
                 for (int rt = 0; rt < NRT; ++rt)
-                    if (rt < NRT - 1 || lastv) base[rt * RSTRIDE] = d[w][rt][c];
+                    if ((rt % TPK < TPK - 1 || lastv) && HXG_PW_SKIP_WO < 2) base[R::off(rt)] = d[w][rt][c];
             }
         }
     }
@@ -251,7 +297,7 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
 // trial digit j1.
 template <int S, int P, int L, int A, int B, int NJ2, int NK>
 __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__restrict__ outE, int epar, int j3,
-                                         int I0, int j2lo, const int (&os)[NK], const int (&orr)[NK], int &seq)
+                                         int I0, int kc, int j2lo, const int (&os)[NK], const int (&orr)[NK], int &seq)
 {
     using C = PWCfg<S, P, L>;
     constexpr CPair pp = make_pair_plan(S, A, B);
@@ -263,7 +309,8 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
     constexpr int offB = C::C2::off(B);
     constexpr int C12a = n1a * n2a;
     constexpr int NCOL = n1b * n1a, NCT = (NCOL + 7) / 8;
-    constexpr int NROW = NJ2 * n2a, NRT = (NROW + 7) / 8;
+    using R = PWRows<NJ2, C::K, n1a, n2a>;
+    constexpr int NRT = R::NRT, TPK = R::TPK;
     constexpr int CTW = C::ctw(A, B);
     static_assert(NRT <= C::RTM && NJ2 <= RJ && 8 % NJ2 == 0, "group shape");
     const int lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
@@ -290,15 +337,18 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
         // diagonal unit (a == b, i3 == j3): I >= J <=> i1 + n1a i2 >= J - I0 = j1 + n1a (j2 - i20) ...
         ln.thr0 = Jb - I0 - i20 * n1a;
         if (!(A == B && Jb + n1b - 1 >= I0)) ln.thr0 = -(1 << 30);
+        ln.kc = kc;
     }
 
     // ---------------- stage B: B_h[r][l] on DMMA -> stage-C A fragments ----------------
     __syncwarp();  // previous group's stage C has read sB
 #pragma unroll 1
     for (int rt = 0; rt < NRT; ++rt) {
-        const int row = rt * 8 + g8;
-        const bool rv = row < NROW;
-        const int jj2 = row & (NJ2 - 1), i2 = rv ? row / NJ2 : 0;
+        __syncwarp();  // converged for the DMMAs after the previous tile's divergent stores
+        const int kk = rt / TPK, row = (rt - kk * TPK) * 8 + g8;  // row inside digit kk's block
+        const int jj2 = row & (NJ2 - 1);
+        const bool rv = row < R::NROWK && kk < kc;  // missing rows / digits beyond kc: zero
+        const int i2 = rv ? row / NJ2 : 0;
         const int j2 = j2lo + jj2;
 #pragma unroll
         for (int h = 0; h < pp.nh; ++h) {
@@ -310,7 +360,9 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
                 if (pp.g_h[g] != h) continue;
                 const double *Ta = sT + (pp.g_fr[g] * KT + i2 + sha1) * LP;
                 const double *Tb = sT + (pp.g_fs[g] * KT + j2 + shb1) * LP;
-                const double *Ag = sA + g * LT * LQ * 32 + lane;
+                // B operand (Abar_kk) is shared by the tile's rows: every lane loads its
+                // column of the tile's digit kk, rows that do not exist included
+                const double *Ag = sA + (kk * C::NG + g) * LT * LQ * 32 + lane;
 #pragma unroll
                 for (int ks = 0; ks < LQ; ++ks) {
                     const int m = ks * 4 + t4;
@@ -330,6 +382,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
                         sB[(rt * NKS + (k >> 2)) * 32 + g8 * 4 + (k & 3)] = d[lt][c];
                     }
                 }
+            __syncwarp();
         }
     }
     __syncwarp();
@@ -348,7 +401,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
             jnext = n1b;
         }
         // trial digits completed by this step: one bulk copy per segment (j1, jj2)
-        if (!pw_direct(S) && jnext > jdone) {
+        if (!pw_direct(S) && jnext > jdone && !HXG_PW_SKIP_WO) {
             fence_proxy_async();
             __syncwarp();
             for (int j1 = jdone; j1 < jnext; ++j1) {
@@ -359,7 +412,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
                     const int cs = J > I0 ? J - I0 : 0;
                     const double *src = slot + ((epar + goff) & 1) + cs;
                     double *dst = outE + goff + cs;
-                    int len = C12a - cs;
+                    int len = kc * C12a - cs;
                     if (reinterpret_cast<size_t>(dst) & 8) {
                         __stcs(dst, *src);
                         ++dst;
@@ -375,7 +428,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
             jdone = jnext;
         }
     }
-    if constexpr (!pw_direct(S)) seq = (seq + n1b) % NSLOT;
+    if constexpr (!pw_direct(S)) seq += n1b;  // sequence numbers of completed trial digits
 }
 
 template <int S, int P, int L, int A, int B>
@@ -385,6 +438,7 @@ __device__ __forceinline__ void pw_unit(const double *sT, double *W, const doubl
     using C = PWCfg<S, P, L>;
     constexpr CPair pp = make_pair_plan(S, A, B);
     constexpr int LP = C::LP, L3 = C::L3, LQ = C::LQ, LT = C::LT, RJ = C::RJ;
+    const int kc = cmin(C::K, C::n(A, 2) - i3);  // test digits i3 .. i3 + kc - 1 of this unit
     constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1), n2b = C::n(B, 1);
     constexpr int sha0 = sh_of(S, A, 0), sha2 = sh_of(S, A, 2);
     constexpr int shb0 = sh_of(S, B, 0), shb2 = sh_of(S, B, 2);
@@ -394,54 +448,65 @@ __device__ __forceinline__ void pw_unit(const double *sT, double *W, const doubl
     double *sP = W + C::W_P, *sA = W + C::W_A;
 
     // ---------------- stage A: contract xi3 -> Abar_g (stage-B B-fragment order) ----------------
+    // for the unit's kc test digits at once: the metric values of a term do not depend
+    // on i3, so each is loaded once and contracted with kc 1D products
+    constexpr int K = C::K;
     __syncwarp();
-    for (int o = lane; o < pp.nt * LP; o += 32) {
-        const int t = o / LP, nn = o - t * LP;
+    for (int o = lane; o < K * pp.nt * LP; o += 32) {
+        const int kk = o / (pp.nt * LP), o2 = o - kk * (pp.nt * LP);
+        const int t = o2 / LP, nn = o2 - t * LP;
         int fr = 0, fs = 0;
 #pragma unroll
         for (int tt = 0; tt < pp.nt; ++tt)
             if (tt == t) { fr = pp.t_fr[tt]; fs = pp.t_fs[tt]; }
-        sP[o] = sT[(fr * KT + i3 + sha2) * LP + nn] * sT[(fs * KT + j3 + shb2) * LP + nn];
+        const int i3k = cmin(i3 + kk, C::n(A, 2) - 1);
+        sP[o] = sT[(fr * KT + i3k + sha2) * LP + nn] * sT[(fs * KT + j3 + shb2) * LP + nn];
     }
     __syncwarp();
     constexpr int NPASS = (L * L + 31) / 32;
 #pragma unroll
     for (int g = 0; g < pp.ng; ++g) {
-        double acc[NPASS];
+        double acc[K][NPASS];
 #pragma unroll
-        for (int q = 0; q < NPASS; ++q) acc[q] = 0.0;
+        for (int kk = 0; kk < K; ++kk)
+#pragma unroll
+            for (int q = 0; q < NPASS; ++q) acc[kk][q] = 0.0;
 #pragma unroll
         for (int t = 0; t < pp.nt; ++t) {
             if (pp.t_g[t] != g) continue;
             const double *Mf = M + pp.t_field[t] * L3;
-            const double *pt = sP + t * LP;
-            double v[NPASS][L];
+            // one pass of 32 points at a time (L values per lane in flight): keeps the
+            // register count low enough for 4 warps per scheduler
 #pragma unroll
             for (int q = 0; q < NPASS; ++q) {
                 const int lm = cmin(lane + 32 * q, L * L - 1);
+                double v[L];
 #pragma unroll
-                for (int nn = 0; nn < L; ++nn) v[q][nn] = __ldg(Mf + nn * L * L + lm);
+                for (int nn = 0; nn < L; ++nn) v[nn] = __ldg(Mf + nn * L * L + lm);
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+                    const double *pt = sP + (kk * pp.nt + t) * LP;
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int nn = 0; nn < L; nn += 2) {
+                        s0 = fma(v[nn], pt[nn], s0);
+                        if (nn + 1 < L) s1 = fma(v[nn + 1], pt[nn + 1], s1);
+                    }
+                    acc[kk][q] += pp.t_sign[t] > 0 ? (s0 + s1) : -(s0 + s1);
+                }
             }
+        }
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk)
 #pragma unroll
             for (int q = 0; q < NPASS; ++q) {
-                double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-                for (int nn = 0; nn < L; nn += 2) {
-                    s0 = fma(v[q][nn], pt[nn], s0);
-                    if (nn + 1 < L) s1 = fma(v[q][nn + 1], pt[nn + 1], s1);
+                const int lm = lane + 32 * q;
+                if (lm < L * L) {
+                    const int l = lm / L, m = lm - l * L;
+                    // B fragment of tile (lt = l / 8, ks = m / 4): lane' = (l % 8) * 4 + m % 4
+                    sA[(((kk * C::NG + g) * LT + (l >> 3)) * LQ + (m >> 2)) * 32 + (l & 7) * 4 + (m & 3)] = acc[kk][q];
                 }
-                acc[q] += pp.t_sign[t] > 0 ? (s0 + s1) : -(s0 + s1);
             }
-        }
-#pragma unroll
-        for (int q = 0; q < NPASS; ++q) {
-            const int lm = lane + 32 * q;
-            if (lm < L * L) {
-                const int l = lm / L, m = lm - l * L;
-                // B fragment of tile (lt = l / 8, ks = m / 4): lane' = (l % 8) * 4 + m % 4
-                sA[((g * LT + (l >> 3)) * LQ + (m >> 2)) * 32 + (l & 7) * 4 + (m & 3)] = acc[q];
-            }
-        }
     }
     __syncwarp();
 
@@ -468,16 +533,16 @@ __device__ __forceinline__ void pw_unit(const double *sT, double *W, const doubl
     while (j2lo < n2b) {
         const int rem = n2b - j2lo;
         if (RJ >= 8 && rem >= 8) {
-            if constexpr (RJ >= 8) pw_group<S, P, L, A, B, 8>(sT, W, outE, epar, j3, I0, j2lo, os, orr, seq);
+            if constexpr (RJ >= 8) pw_group<S, P, L, A, B, 8>(sT, W, outE, epar, j3, I0, kc, j2lo, os, orr, seq);
             j2lo += 8;
         } else if (RJ >= 4 && rem >= 4) {
-            if constexpr (RJ >= 4) pw_group<S, P, L, A, B, 4>(sT, W, outE, epar, j3, I0, j2lo, os, orr, seq);
+            if constexpr (RJ >= 4) pw_group<S, P, L, A, B, 4>(sT, W, outE, epar, j3, I0, kc, j2lo, os, orr, seq);
             j2lo += 4;
         } else if (RJ >= 2 && rem >= 2) {
-            if constexpr (RJ >= 2) pw_group<S, P, L, A, B, 2>(sT, W, outE, epar, j3, I0, j2lo, os, orr, seq);
+            if constexpr (RJ >= 2) pw_group<S, P, L, A, B, 2>(sT, W, outE, epar, j3, I0, kc, j2lo, os, orr, seq);
             j2lo += 2;
         } else {
-            pw_group<S, P, L, A, B, 1>(sT, W, outE, epar, j3, I0, j2lo, os, orr, seq);
+            pw_group<S, P, L, A, B, 1>(sT, W, outE, epar, j3, I0, kc, j2lo, os, orr, seq);
             j2lo += 1;
         }
     }
@@ -495,17 +560,21 @@ __device__ __forceinline__ void pw_run_unit(int u, const double *sT, double *W, 
         for (int a = b; a < C::NB; ++a) {
             if (pair < 0) {
                 const int n3b = C::n(b, 2), n3a = C::n(a, 2);
-                const int cnt = a == b ? n3b * (n3b + 1) / 2 : n3b * n3a;
+                int cnt = 0;  // units of the pair: test digits i3 in blocks of K
+                if (a == b)
+                    for (int jj = 0; jj < n3b; ++jj) cnt += C::kcnt(n3a - jj);
+                else
+                    cnt = n3b * C::kcnt(n3a);
                 if (rem < cnt) {
                     pair = a * 3 + b;
-                    if (a == b) {  // j3 <= i3 < n3
+                    if (a == b) {  // j3 <= i3 < n3, i3 = j3 + K r
                         int jj = 0, r = rem;
-                        while (r >= n3a - jj) { r -= n3a - jj; ++jj; }
+                        while (r >= C::kcnt(n3a - jj)) { r -= C::kcnt(n3a - jj); ++jj; }
                         j3 = jj;
-                        i3 = jj + r;
+                        i3 = jj + C::K * r;
                     } else {
-                        j3 = rem / n3a;
-                        i3 = rem - j3 * n3a;
+                        j3 = rem / C::kcnt(n3a);
+                        i3 = C::K * (rem - j3 * C::kcnt(n3a));
                     }
                 } else {
                     rem -= cnt;
@@ -532,7 +601,7 @@ __device__ __forceinline__ void pw_run_unit(int u, const double *sT, double *W, 
 // down to one unit (small batches fill the GPU too), and the CTAs' elements
 // stay few at a time (the metric of an element is read from L2 by its units).
 template <int S, int P, int L>
-__global__ void __launch_bounds__(PW_THREADS, (PWCfg<S, P, L>::MINB))
+__global__ void __launch_bounds__(PWCfg<S, P, L>::THREADS, (PWCfg<S, P, L>::MINB))
     general_pw_kernel(const __grid_constant__ PWArgs args)
 {
     using C = PWCfg<S, P, L>;
@@ -540,7 +609,7 @@ __global__ void __launch_bounds__(PW_THREADS, (PWCfg<S, P, L>::MINB))
     __shared__ int s_next;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double *sT = smem + C::OFF_T;
-    for (int idx = threadIdx.x; idx < 2 * KT * C::LP; idx += PW_THREADS) {
+    for (int idx = threadIdx.x; idx < 2 * KT * C::LP; idx += C::THREADS) {
         const int fk = idx / C::LP, l = idx - fk * C::LP;
         sT[idx] = l < L ? args.tables[TAB_T + fk * LT + l] : 0.0;
     }

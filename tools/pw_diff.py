@@ -14,11 +14,16 @@ sys.path.insert(0, ROOT)
 
 
 def digits(space, p, I):
-    from paper_1711_00984_b200.inputs import dim
+    """(block, d1, d2, d3) of flat index I (spaces.py:9-17 layout)"""
     if space in ("H1", "L2"):
         n = p + 1 if space == "H1" else p
         return (0, I % n, (I // n) % n, I // (n * n))
-    raise NotImplementedError
+    for a in range(3):
+        ext = [(p + 1 if d == a else p) if space == "Hdiv" else (p if d == a else p + 1) for d in range(3)]
+        sz = ext[0] * ext[1] * ext[2]
+        if I < sz:
+            return (a, I % ext[0], (I // ext[0]) % ext[1], I // (ext[0] * ext[1]))
+        I -= sz
 
 
 def main():
@@ -48,7 +53,7 @@ def main():
     if bad.shape[0]:
         rows, cols = iu[0][bad[:, 1]], iu[1][bad[:, 1]]
         out["nan"] = int(np.isnan(got).sum())
-        if space in ("H1", "L2"):
+        if True:
             dj = np.array([digits(space, p, int(r)) for r in rows[:4000]])
             di = np.array([digits(space, p, int(c)) for c in cols[:4000]])
             for k, nm in ((1, "j1"), (2, "j2"), (3, "j3")):
@@ -56,6 +61,7 @@ def main():
             for k, nm in ((1, "i1"), (2, "i2"), (3, "i3")):
                 out["bad_" + nm] = sorted(set(int(x) for x in di[:, k]))
             out["bad_j3i3"] = sorted(set((int(x), int(y)) for x, y in zip(dj[:, 3], di[:, 3])))[:40]
+            out["bad_blocks"] = sorted(set((int(x), int(y)) for x, y in zip(dj[:, 0], di[:, 0])))
         out["sample"] = [(int(r), int(c), float(got[e, k]), float(ref[e, k])) for (e, k), r, c in
                          list(zip(bad[:6], rows[:6], cols[:6]))]
     print(json.dumps(out))
