@@ -393,6 +393,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 constexpr int NLT = (L + 7) / 8, LQ = (L + 3) / 4;
                 const int nrt = (r2 * n2a + 7) >> 3;
                 for (int w = warp; w < (HXG_V2_SKIP & 2 ? 0 : pp.nh * r3 * nrt); w += V2_WARPS) {
+                    __syncwarp();  // converged for mma.sync (.aligned) after divergent code
                     const int h = w / (r3 * nrt), w2 = w - h * (r3 * nrt);
                     const int ii3 = w2 / nrt, rt = w2 - ii3 * nrt;
                     const int row = rt * 8 + g8;
@@ -497,6 +498,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 int ko[NKS];
                 int ctc = -1, dj1 = -1, di1 = 0;
                 for (int it = it0; it < it1; ++it) {
+                    __syncwarp();  // converged for mma.sync (.aligned) after divergent code
                     const int ct = it / nrtp, rt0 = RT * (it - ct * nrtp);
                     if (ct != ctc) {  // (re)load the B fragment of column tile ct
                         ctc = ct;
@@ -561,6 +563,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 int bo[NKS];
                 int ctn = it0 / r2, jj2 = it0 - ctn * r2;  // tiles (ct, jj2), jj2 fastest
                 for (int it = it0; it < it1; ++it) {
+                    __syncwarp();  // converged for mma.sync (.aligned) after divergent code
                     if (ctn != ct) {
                         ct = ctn;
                         const int c = ct * 8 + g8;
@@ -633,6 +636,7 @@ __device__ __forceinline__ void v2_process(const V2Args &args, double *smem, int
                 int qd = it0 / r2, jj2 = it0 - qd * r2;
                 int ii3 = qd / n2a, i2 = qd - ii3 * n2a;
                 for (int it = it0; it < it1; ++it) {
+                    __syncwarp();  // converged for mma.sync (.aligned) after divergent code
                     const double *base = sB + jj2 * SJ2 + (ii3 * N2 + i2) * LP;
                     double d0 = 0.0, d1 = 0.0;
 #pragma unroll

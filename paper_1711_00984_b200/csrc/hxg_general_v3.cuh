@@ -352,6 +352,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
         if constexpr (YF) {
 #pragma unroll
             for (int i2 = 0; i2 < n2a; i2 += kTF) {  // kTF tiles (i2, i2 + 1, ...) in flight
+                __syncwarp();  // converged for mma.sync (.aligned) after the previous iteration's divergent stores
                 double d[kTF][2];
 #pragma unroll
                 for (int c = 0; c < kTF; ++c) d[c][0] = d[c][1] = 0.0;
@@ -378,6 +379,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
         } else {
 #pragma unroll
             for (int i1 = 0; i1 < n1a; i1 += kTF) {  // kTF tiles (i1, i1 + 1, ...) in flight
+                __syncwarp();  // converged for mma.sync (.aligned) after the previous iteration's divergent stores
                 double d[kTF][2];
 #pragma unroll
                 for (int c = 0; c < kTF; ++c) d[c][0] = d[c][1] = 0.0;

@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(GEN_THREADS, (LMAX <= 8 ? 2 : 1))
                         }
                     }
                     for (int jj2 = 0; jj2 < r2; ++jj2) {
+                        __syncwarp();  // converged for mma.sync (.aligned) after divergent code
                         const double *sBj = sB + jj2 * SJ2;
                         double d[NMT][2];
 #pragma unroll
