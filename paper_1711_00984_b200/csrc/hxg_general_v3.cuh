@@ -26,6 +26,9 @@ namespace hxg {
 #ifndef HXG_V3_DEBUG_EMIN
 #define HXG_V3_DEBUG_EMIN 0
 #endif
+#ifndef HXG_V3_AFRAG
+#define HXG_V3_AFRAG 1  // Abar in stage-B fragment order (0: row-major [m][l], 2-way bank conflicts)
+#endif
 #ifndef HXG_V3_TF
 #define HXG_V3_TF 4
 #endif
@@ -223,7 +226,9 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
             const int lm = lane + 32 * q;
             if (lm < L * L) {
                 const int l = lm / L, m = lm - l * L;
-                sAk[(g * 8 + m) * 8 + l] = acc[q];
+                // stage-B B fragment order (k = m, n = l): conflict-free 8-byte loads
+                if constexpr (HXG_V3_AFRAG) sAk[g * 64 + (m >> 2) * 32 + l * 4 + (m & 3)] = acc[q];
+                else sAk[(g * 8 + m) * 8 + l] = acc[q];
             }
         }
     }
@@ -327,7 +332,7 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
                     const int g = (h0 + c < MAXH) ? GL.g[h0 + c][q / LQ] : -1, ks = q % LQ;
                     if (h0 + c < pp.nh && g >= 0) {
                         const double av = Ta[pp.g_fr[g]][ks] * Tb[pp.g_fs[g]][ks];
-                        const double bv = sAk[(g * 8 + ks * 4 + t4) * 8 + g8];
+                        const double bv = HXG_V3_AFRAG ? sAk[g * 64 + ks * 32 + lane] : sAk[(g * 8 + ks * 4 + t4) * 8 + g8];
                         dmma_8x8x4_keep(d[c][0], d[c][1], av, bv, keep);
                     }
                 }
@@ -335,8 +340,8 @@ __device__ __forceinline__ void v3_unit(const V3Args &args, const double *sT, do
 #pragma unroll
             for (int c = 0; c < 2; ++c)
                 if (h0 + c < pp.nh) {
-                    sBw[((h0 + c) * 8 + g8) * 8 + 2 * t4] = d[c][0];
-                    sBw[((h0 + c) * 8 + g8) * 8 + 2 * t4 + 1] = d[c][1];
+                    // one 16-byte store per lane (a row of 8 doubles per g8: 4 wavefronts, no conflicts)
+                    *reinterpret_cast<double2 *>(sBw + ((h0 + c) * 8 + g8) * 8 + 2 * t4) = make_double2(d[c][0], d[c][1]);
                 }
         }
         __syncwarp();
