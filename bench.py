@@ -175,8 +175,8 @@ def gather_checksums(out, world, device=None):
     import torch
 
     E = out.shape[0]
-    o = out.to(torch.float64)
-    loc = torch.stack([o.sum(), (o * o).sum(), torch.linalg.norm(o[0]), torch.linalg.norm(o[E - 1]),
+    o = out.reshape(-1)  # fp64 already; reductions only (no output-sized temporaries: 100 GB sweeps)
+    loc = torch.stack([o.sum(), torch.dot(o, o), torch.linalg.norm(out[0]), torch.linalg.norm(out[E - 1]),
                        torch.tensor(float(E), dtype=torch.float64, device=o.device)])
     if world == 1:
         return [loc.tolist()]

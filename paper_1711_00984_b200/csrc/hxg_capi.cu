@@ -334,9 +334,17 @@ static bool ext_gather_route(int path, int p1, int p2, int p3, int L)
     return path == EXTRUSION && !(p1 == p2 && p2 == p3) && L < p1 + 1;
 }
 
+// the specialized metric kernel covers L = 2..11 and writes every status word itself
+static bool metric_v2_ok(int space, int L)
+{
+    const char *fg = getenv("HXG_FORCE_GENERIC");
+    return space >= 0 && space <= 3 && L >= 2 && L <= 11 && !(fg && fg[0] == '1');
+}
+
 static int metric_run(int space, int p1, int p2, int p3, int L, int E, const int *kind,
                        const double *params, const double *coef, const double *wgrid,
-                       const double *tables, double *metric, int *status, void *stream)
+                       const double *tables, double *metric, int *status, void *stream,
+                       bool status_whole)
 {
     int rc = check_common(space, GENERAL, p1, p2, p3, L, E);
     if (rc != HXG_OK) return rc;
@@ -345,6 +353,19 @@ static int metric_run(int space, int p1, int p2, int p3, int L, int E, const int
     SpacePlan P;
     rc = build_plan(space, p1, p2, p3, P);
     if (rc != HXG_OK) return rc;
+    // compile-time specialized kernel (writes whole status words) unless the generic one is forced
+    const char *fg = getenv("HXG_FORCE_GENERIC");
+    if (metric_v2_ok(space, L) && !(fg && fg[0] == '1')) {
+        MetArgs a{E, kind, params, coef, wgrid, tables, metric, status, status_whole ? 0 : 1};
+        int r = 1;
+        switch (space) {
+        case H1: r = launch_met_H1(L, a, (cudaStream_t)stream); break;
+        case HCURL: r = launch_met_hcurl(L, a, (cudaStream_t)stream); break;
+        case HDIV: r = launch_met_hdiv(L, a, (cudaStream_t)stream); break;
+        case L2: r = launch_met_l2(L, a, (cudaStream_t)stream); break;
+        }
+        if (r <= 0) return r == 0 ? HXG_OK : HXG_ERR_CUDA;
+    }
     const long long npts = (long long)E * L * L * L;
     const int mgrid = (int)std::min<long long>((npts + 255) / 256, (long long)sm_count() * 64);
     metric_kernel<<<mgrid, 256, 0, (cudaStream_t)stream>>>(space, L, E, kind, params, coef, wgrid,
@@ -449,7 +470,14 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
     const char *force_generic = getenv("HXG_FORCE_GENERIC");
     const bool aff_spec = path == AFFINE && p1 == p2 && p2 == p3 && p1 <= 10 &&
                           !(force_generic && force_generic[0] == '1');
-    if (!aff_spec && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
+    // general path, unfused orders: the specialized metric kernel writes the words whole
+    const char *force_v2 = getenv("HXG_FORCE_V2");
+    const bool fused_gen = path == GENERAL && p1 == p2 && p2 == p3 && p1 <= 3 && L == p1 + 1 &&
+                           !(force_generic && force_generic[0] == '1') && !(force_v2 && force_v2[0] == '1');
+    const bool met_writes = path == GENERAL && !fused_gen && metric_v2_ok(space, L) &&
+                            !ext_gather_route(path, p1, p2, p3, L);
+    if (!aff_spec && !met_writes && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess)
+        return HXG_ERR_CUDA;
 
     if (path == AFFINE) {
         const char *force = force_generic;
@@ -624,7 +652,7 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
         double *metric = (double *)workspace;
         rc = metric_run(space, p1, p2, p3, L, ne, kind + e0, params + 24 * e0,
                                 coef ? coef + e0 : nullptr, wgrid ? wgrid + e0 * L * L * L : nullptr,
-                                tables, metric, status + e0, stream);
+                                tables, metric, status + e0, stream, met_writes);
         if (rc != HXG_OK) return rc;
         rc = hxg_contract_batched(space, p1, p2, p3, L, ne, tables, metric, out + e0 * Pk, stream);
         if (rc != HXG_OK) return rc;
@@ -636,10 +664,11 @@ int hxg_metric_batched(int space, int p1, int p2, int p3, int L, int E, const in
                        const double *params, const double *coef, const double *wgrid,
                        const double *tables, double *metric, int *status, void *stream)
 {
-    // exported entry: the status word is written by the call (zeroed, then ORed)
-    if (E > 0 && status && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, (cudaStream_t)stream) != cudaSuccess)
+    // exported entry: the status word is written by the call (zeroed, then ORed; the
+    // specialized metric kernel writes it whole)
+    if (E > 0 && status && !metric_v2_ok(space, L) && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, (cudaStream_t)stream) != cudaSuccess)
         return HXG_ERR_CUDA;
-    return metric_run(space, p1, p2, p3, L, E, kind, params, coef, wgrid, tables, metric, status, stream);
+    return metric_run(space, p1, p2, p3, L, E, kind, params, coef, wgrid, tables, metric, status, stream, true);
 }
 
 int hxg_contract_batched(int space, int p1, int p2, int p3, int L, int E, const double *tables,

@@ -12,6 +12,7 @@
 #include "hxg_general_v2.cuh"
 #include "hxg_general_v3.cuh"
 #include "hxg_general_pw.cuh"
+#include "hxg_metric.cuh"
 #include "hxg_v2_launch.h"
 
 namespace hxg {
@@ -164,6 +165,24 @@ int aff_launch(int p, const AffV2Args &a, cudaStream_t st)
     return 1;
 }
 
+template <int S>
+int met_launch(int L, const MetArgs &a, cudaStream_t st)
+{
+    const unsigned grid = (unsigned)((a.E + MET2_WARPS - 1) / MET2_WARPS);
+    switch (L) {
+#define HXG_MCASE(LL)                                                                                      \
+    case LL:                                                                                               \
+        metric_v2_kernel<S, LL><<<grid, MET2_WARPS * 32, 0, st>>>(a.E, a.kind, a.params, a.coef, a.wgrid, \
+                                                                  a.tables, a.metric, a.status,           \
+                                                                  a.status_or);                           \
+        return cudaGetLastError() == cudaSuccess ? 0 : -5;
+        HXG_MCASE(2) HXG_MCASE(3) HXG_MCASE(4) HXG_MCASE(5) HXG_MCASE(6)
+        HXG_MCASE(7) HXG_MCASE(8) HXG_MCASE(9) HXG_MCASE(10) HXG_MCASE(11)
+#undef HXG_MCASE
+    }
+    return 1;
+}
+
 // specialized extrusion-map kernel (simp_*_ext); returns 1 if none exists for p
 template <int S>
 int ext_launch(int p, const ExtArgs &a, cudaStream_t st)
@@ -188,4 +207,5 @@ int ext_launch(int p, const ExtArgs &a, cudaStream_t st)
     int HXG_GEN_CAT(launch_v2_, NAME)(int p, const V2Args &a, cudaStream_t st) { return gen_launch<SPACE>(p, a, st); } \
     int HXG_GEN_CAT(launch_aff_, NAME)(int p, const AffV2Args &a, cudaStream_t st) { return aff_launch<SPACE>(p, a, st); } \
     int HXG_GEN_CAT(launch_ext_, NAME)(int p, const ExtArgs &a, cudaStream_t st) { return ext_launch<SPACE>(p, a, st); } \
+    int HXG_GEN_CAT(launch_met_, NAME)(int L, const MetArgs &a, cudaStream_t st) { return met_launch<SPACE>(L, a, st); } \
     }
