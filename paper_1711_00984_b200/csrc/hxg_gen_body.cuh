@@ -23,12 +23,10 @@ static inline bool env_on(const char *name)
     return v && v[0] == '1';
 }
 
-// general_v3_kernel<H1, 7, 8> was routed to v2 in round 1 after wrong results
-// under ptxas -O3.  On the current source it is
-// correct (tools/v3p7_check.py: 64 elements vs the oracle at 3e-16, with and
-// without the HXG_DMMA_KEEP register hack; tests/test_gpu_parity.py sweeps) and
-// 1.65x faster than v2 (profiles/v3p7_r02.txt), so it runs by default;
-// HXG_V3_P7=0 restores the v2 route.
+// general_v3_kernel<H1, 7, 8> was routed to v2 in round 1 after wrong results under
+// ptxas -O3; the cause was a missing warp reconvergence before mma.sync (DESIGN.md
+// "Warp reconvergence before mma.sync"), and the kernel runs by default (1.65x over v2,
+// profiles/v3p7_r02.txt).  HXG_V3_P7=0 restores the v2 route.
 template <int S, int P>
 bool v3_enabled()
 {
@@ -39,10 +37,9 @@ bool v3_enabled()
     return true;
 }
 
-// warp-owned P-form kernel (hxg_general_pw.cuh): default for p >= 8 (digit
-// extents 9-11, where the v3 8x8 tiles do not fit and v2's CTA-chunked stages
-// stall at barriers) in H1 and H(curl), and for H(div) at p = 8; measured
-// (profiles/pw_r02.txt) v2 stays ahead for H(div) p = 9, 10 and is kept for L2.
+// warp-owned P-form kernel (hxg_general_pw.cuh): default for p >= 8 (digit extents
+// 9-11, where the v3 8x8 tiles do not fit and v2's CTA-chunked stages stall at
+// barriers) in H1, H(curl) and H(div) (profiles/sweep_r02.json); L2 keeps v2.
 // HXG_PW=1 selects it for every order it supports, HXG_PW=0 never.
 template <int S, int P>
 bool pw_enabled()
