@@ -175,9 +175,16 @@ def gather_checksums(out, world, device=None):
     import torch
 
     E = out.shape[0]
-    o = out.reshape(-1)  # fp64 already; reductions only (no output-sized temporaries: 100 GB sweeps)
-    loc = torch.stack([o.sum(), torch.dot(o, o), torch.linalg.norm(out[0]), torch.linalg.norm(out[E - 1]),
-                       torch.tensor(float(E), dtype=torch.float64, device=o.device)])
+    # reductions only, in row blocks (no output-sized temporaries, no 2^31 BLAS limit: 100 GB sweeps)
+    rows = max(1, (1 << 28) // max(1, out.shape[1]))
+    s1 = torch.zeros((), dtype=torch.float64, device=out.device)
+    s2 = torch.zeros((), dtype=torch.float64, device=out.device)
+    for r0 in range(0, E, rows):
+        blk = out[r0:r0 + rows].reshape(-1)
+        s1 += blk.sum()
+        s2 += torch.dot(blk, blk)
+    loc = torch.stack([s1, s2, torch.linalg.norm(out[0]), torch.linalg.norm(out[E - 1]),
+                       torch.tensor(float(E), dtype=torch.float64, device=out.device)])
     if world == 1:
         return [loc.tolist()]
     import torch.distributed as dist

@@ -65,8 +65,15 @@ int gen_launch_one(const V2Args &a, cudaStream_t st)
             b.out = a.out;
             b.P = a.P;
             b.E = a.E;
+            // CTA c takes the item range [c T / G, (c + 1) T / G) of the T = E * NU (element,
+            // unit) items; G = one wave (measured best: H1 p8 73 % vs 60-69 % with 1-8 CTAs
+            // per element left to the block scheduler), or HXG_PW_DIV CTAs per element
             const long long items = (long long)a.E * CP::NU;
-            const int grid = (int)std::min<long long>(items, (long long)sm_count() * CP::MINB);
+            const char *dv = getenv("HXG_PW_DIV");
+            const int div = dv ? atoi(dv) : 0;
+            const long long wave = (long long)sm_count() * CP::MINB;
+            const long long g = div > 0 ? std::max<long long>(wave, (long long)a.E * div) : wave;
+            const int grid = (int)std::min<long long>(items, std::min<long long>(g, 1ll << 30));
             kp<<<grid, CP::THREADS, CP::SMEM_BYTES, st>>>(b);
             return cudaGetLastError() == cudaSuccess ? 0 : -5;
         }
