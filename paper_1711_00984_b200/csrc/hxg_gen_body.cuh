@@ -128,8 +128,12 @@ int gen_launch(int p, const V2Args &a, cudaStream_t st)
 {
     switch (p) {
 #define HXG_CASE(PP) case PP: return gen_launch_one<S, PP>(a, st);
+#ifdef HXG_QUICK_PS  // experiment builds (tools/variant_tu.sh): only these orders
+        HXG_QUICK_PS
+#else
         HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
         HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#endif
 #undef HXG_CASE
     }
     return 1;
@@ -162,8 +166,10 @@ int aff_launch(int p, const AffV2Args &a, cudaStream_t st)
 {
     switch (p) {
 #define HXG_CASE(PP) case PP: return aff_launch_one<S, PP>(a, st);
+#ifndef HXG_QUICK_PS
         HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
         HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#endif
 #undef HXG_CASE
     }
     return 1;
@@ -193,8 +199,10 @@ int ext_launch(int p, const ExtArgs &a, cudaStream_t st)
 {
     switch (p) {
 #define HXG_CASE(PP) case PP: return launch_ext_t<S, PP>(a, st);
+#ifndef HXG_QUICK_PS
         HXG_CASE(1) HXG_CASE(2) HXG_CASE(3) HXG_CASE(4) HXG_CASE(5)
         HXG_CASE(6) HXG_CASE(7) HXG_CASE(8) HXG_CASE(9) HXG_CASE(10)
+#endif
 #undef HXG_CASE
     }
     return 1;

@@ -68,6 +68,13 @@ __host__ __device__ constexpr bool pw_direct(int S) { return HXG_PW_WO < 0 ? (S 
 #ifndef HXG_PW_SKIP_WO
 #define HXG_PW_SKIP_WO 0  // timing experiment only (wrong results): 1 no copy-out, 2 no staging either
 #endif
+// stage-C A operand (B_h fragments of the group's row tiles) held in registers for the
+// whole group instead of re-read from shared memory at every column tile: -1 (default) =
+// for the staged (HBM-bound) spaces, 0 never, 1 always
+#ifndef HXG_PW_ASTAT
+#define HXG_PW_ASTAT -1
+#endif
+__host__ __device__ constexpr bool pw_astat(int S) { return HXG_PW_ASTAT < 0 ? !pw_direct(S) : HXG_PW_ASTAT == 1; }
 constexpr int PW_WARPS = HXG_PW_WARPS;
 constexpr int PW_THREADS = PW_WARPS * 32;
 
@@ -211,9 +218,10 @@ struct PWLane {
 
 // One stage-C step: CTW column tiles starting at column tile ct, all row tiles of the
 // group, then the staging stores of this lane's D fragments.
-template <int S, int P, int L, int A, int B, int NJ2, int NK, int CTW>
+template <int S, int P, int L, int A, int B, int NJ2, int NK, int CTW, int NRTA>
 __device__ __forceinline__ void pw_step(const double *sT, const double *sB, double *sS, int ct, int seq,
-                                        const int (&os)[NK], const int (&orr)[NK], const PWLane &ln)
+                                        const int (&os)[NK], const int (&orr)[NK], const PWLane &ln,
+                                        const double (&areg)[NRTA][NK])
 {
     using C = PWCfg<S, P, L>;
     constexpr int LP = C::LP, NKS = C::NKS, SEG = C::SEG, NSLOT = C::NSLOT, RJ = C::RJ;
@@ -245,7 +253,9 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
     for (int ks = 0; ks < NK; ++ks)
 #pragma unroll
         for (int rt = 0; rt < NRT; ++rt) {
-            const double a = sB[(rt * NKS + ks) * 32 + lane];
+            double a;
+            if constexpr (pw_astat(S)) a = areg[rt][ks];
+            else a = sB[(rt * NKS + ks) * 32 + lane];
 #pragma unroll
             for (int w = 0; w < CTW; ++w) dmma_8x8x4(d[w][rt][0], d[w][rt][1], a, Bp[w][ks]);
         }
@@ -387,6 +397,16 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
     }
     __syncwarp();
     // ---------------- stage C: P-form on DMMA, column tiles in j1 order ----------------
+    constexpr int NRTA = pw_astat(S) ? NRT : 1;
+    double areg[NRTA][NK];
+    if constexpr (pw_astat(S)) {
+#pragma unroll
+        for (int rt = 0; rt < NRT; ++rt)
+#pragma unroll
+            for (int ks = 0; ks < NK; ++ks) areg[rt][ks] = sB[(rt * NKS + ks) * 32 + lane];
+    } else {
+        areg[0][0] = 0.0;
+    }
     int jdone = 0;  // trial digits j1 < jdone have been written out
     constexpr int NST = NCT / CTW;  // full steps; an odd NCT ends with one single-tile step
 #pragma unroll 1
@@ -394,10 +414,10 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
         const int ct = st * CTW;
         int jnext;
         if (st < NST) {
-            pw_step<S, P, L, A, B, NJ2, NK, CTW>(sT, sB, sS, ct, seq, os, orr, ln);
+            pw_step<S, P, L, A, B, NJ2, NK, CTW>(sT, sB, sS, ct, seq, os, orr, ln, areg);
             jnext = ct + CTW < NCT ? ((ct + CTW) * 8) / n1a : n1b;
         } else {
-            if constexpr (NCT % CTW != 0) pw_step<S, P, L, A, B, NJ2, NK, 1>(sT, sB, sS, ct, seq, os, orr, ln);
+            if constexpr (NCT % CTW != 0) pw_step<S, P, L, A, B, NJ2, NK, 1>(sT, sB, sS, ct, seq, os, orr, ln, areg);
             jnext = n1b;
         }
         // trial digits completed by this step: one bulk copy per segment (j1, jj2)

@@ -11,4 +11,5 @@ python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/re_bench_ref.
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/re_launches.csv \
     python bench.py --no-suite --no-cpu --steps 2 --warmup 3 --e2e-steps -1 > gpurun_out/re_ncu_bench.log 2>&1
 WLS="${WLS:-c2_h1_p5_general:general_v3 c4_hdiv_p7_general:general_v3 c4_l2_p7_general:general_v3}" bash tools/ncu_configs.sh
+bash tools/ncu_digest.sh
 cat gpurun_out/re_tests.txt gpurun_out/re_smoke.txt
