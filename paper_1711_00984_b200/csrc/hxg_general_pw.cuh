@@ -74,6 +74,9 @@ __host__ __device__ constexpr bool pw_direct(int S) { return HXG_PW_WO < 0 ? (S 
 #ifndef HXG_PW_ASTAT
 #define HXG_PW_ASTAT -1
 #endif
+#ifndef HXG_PW_BHOIST
+#define HXG_PW_BHOIST 1  // A-stationary groups: stage-B B fragments and trial-side 1D values in registers
+#endif
 __host__ __device__ constexpr bool pw_astat(int S) { return HXG_PW_ASTAT < 0 ? !pw_direct(S) : HXG_PW_ASTAT == 1; }
 constexpr int PW_WARPS = HXG_PW_WARPS;
 constexpr int PW_THREADS = PW_WARPS * 32;
@@ -137,7 +140,7 @@ struct PWCfg {
     __host__ __device__ static constexpr int rtmax(int rj) { return K * ((rj * C2::N2 + 7) / 8); }
     __host__ __device__ static constexpr int w_tot(int rj)
     {
-        return K * NT * LP + K * NG * LT * LQ * 32 + rtmax(rj) * NKS * 32 + NSLOT_SMEM * rj * SEG;
+        return K * NT * LP + K * NG * LT * LQ * 32 + (pw_astat(S) ? 1 : rtmax(rj)) * NKS * 32 + NSLOT_SMEM * rj * SEG;
     }
     __host__ __device__ static constexpr int cta_bytes(int rj) { return (2 * KT * LP + WARPS * w_tot(rj)) * 8 + 16; }
     // RJCAP: optional cap on the trial digits per group (test hook; the round-2 H1 p = 7
@@ -159,7 +162,7 @@ struct PWCfg {
     static constexpr int W_P = 0;                        // [NT][LP] stage-A 1D products
     static constexpr int W_A = W_P + K * NT * LP;            // [K][NG][LT][LQ][32] Abar (stage-B B fragments)
     static constexpr int W_B = W_A + K * NG * LT * LQ * 32;  // [RTM][NKS][32] B_h (stage-C A fragments)
-    static constexpr int W_S = W_B + RTM * NKS * 32;     // [NSLOT][RJ][SEG] staging
+    static constexpr int W_S = W_B + (pw_astat(S) ? 1 : RTM) * NKS * 32;  // [NSLOT][RJ][SEG] staging
     static constexpr int W_TOT = w_tot(RJ);
     static constexpr int OFF_T = 0;
     static constexpr int OFF_W = 2 * KT * LP;
@@ -214,13 +217,21 @@ struct PWLane {
     int Jb;         // packed row of (j1 = 0, this lane's j2)
     int thr0;       // diagonal units: columns c < J - I0 of row J are below the diagonal (-1 << 30 otherwise)
     int kc;         // test digits of the unit (row tiles of digits kk >= kc are not written)
+    // staged write-out: running column state, advanced by 8 columns per step, instead of
+    // divisions per step
+    int bj1, bi1;        // (j1, i1) of this lane's stage-C B-operand column ct * 8 + g8
+    int sj1[2], si1[2];  // (j1, i1) of this lane's D columns ct * 8 + 2 t4 + c
+    int ssl[2];          // staging slot (seq + sj1) mod NSLOT
+    int ej1, ei1;        // (j1, i1) of column (ct + 1) * 8: trial digits below ej1 are complete
+    // bulk write-out (lanes < NJ2): packed row of the next trial digit to leave
+    int wJ, wgoff, wsl;  // its row, offset of (row, column I0) in the element, staging slot
 };
 
 // One stage-C step: CTW column tiles starting at column tile ct, all row tiles of the
 // group, then the staging stores of this lane's D fragments.
 template <int S, int P, int L, int A, int B, int NJ2, int NK, int CTW, int NRTA>
 __device__ __forceinline__ void pw_step(const double *sT, const double *sB, double *sS, int ct, int seq,
-                                        const int (&os)[NK], const int (&orr)[NK], const PWLane &ln,
+                                        const int (&os)[NK], const int (&orr)[NK], PWLane &ln,
                                         const double (&areg)[NRTA][NK])
 {
     using C = PWCfg<S, P, L>;
@@ -235,14 +246,24 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
     // promise reconvergence there)
     __syncwarp();
     double Bp[CTW][NK];
+    if constexpr (pw_direct(S)) {
 #pragma unroll
-    for (int w = 0; w < CTW; ++w) {
-        // columns beyond NCOL read in-range table rows: their D columns are never stored
-        const int col = cmin((ct + w) * 8 + g8, NCOL - 1);
-        const int j1c = col / n1a, i1c = col - (col / n1a) * n1a;
-        const double *ps = sT + j1c * LP, *pr = sT + i1c * LP;
+        for (int w = 0; w < CTW; ++w) {
+            // columns beyond NCOL read in-range table rows: their D columns are never stored
+            const int col = cmin((ct + w) * 8 + g8, NCOL - 1);
+            const int j1c = col / n1a, i1c = col - (col / n1a) * n1a;
+            const double *ps = sT + j1c * LP, *pr = sT + i1c * LP;
 #pragma unroll
-        for (int ks = 0; ks < NK; ++ks) Bp[w][ks] = ps[os[ks]] * pr[orr[ks]];
+            for (int ks = 0; ks < NK; ++ks) Bp[w][ks] = ps[os[ks]] * pr[orr[ks]];
+        }
+    } else {
+        static_assert(pw_direct(S) || CTW == 1, "staged write-out runs one column tile per step");
+        // columns beyond NCOL (bj1 >= n1b) read an in-range table row: never stored
+        const double *ps = sT + cmin(ln.bj1, n1b - 1) * LP, *pr = sT + ln.bi1 * LP;
+#pragma unroll
+        for (int ks = 0; ks < NK; ++ks) Bp[0][ks] = ps[os[ks]] * pr[orr[ks]];
+        ln.bi1 += 8;
+        while (ln.bi1 >= n1a) { ln.bi1 -= n1a; ++ln.bj1; }
     }
     double d[CTW][NRT][2];
 #pragma unroll
@@ -287,18 +308,21 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
     asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(NSLOT - 1 - C::JSPAN) : "memory");
     __syncwarp();
 #pragma unroll
-    for (int w = 0; w < CTW; ++w)
+    for (int c = 0; c < 2; ++c) {
+        const int j1 = ln.sj1[c], i1 = ln.si1[c];
+        if (j1 < n1b) {
+            double *base = sS + ln.ssl[c] * (RJ * SEG) + ln.rowoff0 + i1 + ((ln.pat >> (j1 & 3)) & 1);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int oc = (ct + w) * 8 + 2 * t4 + c;
-            if (oc < NCOL) {
-                const int j1 = oc / n1a, i1 = oc - (oc / n1a) * n1a;
-                double *base = sS + ((seq + j1) % NSLOT) * (RJ * SEG) + ln.rowoff0 + i1 + ((ln.pat >> (j1 & 3)) & 1);
-#pragma unroll
-                for (int rt = 0; rt < NRT; ++rt)
-                    if ((rt % TPK < TPK - 1 || lastv) && HXG_PW_SKIP_WO < 2) base[R::off(rt)] = d[w][rt][c];
-            }
+            for (int rt = 0; rt < NRT; ++rt)
+                if ((rt % TPK < TPK - 1 || lastv) && HXG_PW_SKIP_WO < 2) base[R::off(rt)] = d[0][rt][c];
         }
+        ln.si1[c] = i1 + 8;
+        while (ln.si1[c] >= n1a) {
+            ln.si1[c] -= n1a;
+            ++ln.sj1[c];
+            ln.ssl[c] = ln.ssl[c] + 1 == NSLOT ? 0 : ln.ssl[c] + 1;
+        }
+    }
     }
 }
 
@@ -348,12 +372,52 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
         ln.thr0 = Jb - I0 - i20 * n1a;
         if (!(A == B && Jb + n1b - 1 >= I0)) ln.thr0 = -(1 << 30);
         ln.kc = kc;
+        // running column state (staged write-out); seq is kept reduced mod NSLOT
+        ln.bj1 = g8 / n1a;
+        ln.bi1 = g8 % n1a;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            ln.sj1[c] = (2 * t4 + c) / n1a;
+            ln.si1[c] = (2 * t4 + c) % n1a;
+            ln.ssl[c] = (seq + ln.sj1[c]) % NSLOT;
+        }
+        ln.ej1 = 8 / n1a;
+        ln.ei1 = 8 % n1a;
+        const int Jw = offB + n1b * (j2lo + lane + n2b * j3);  // lanes < NJ2 own trial digit jj2 = lane
+        ln.wJ = Jw;
+        ln.wgoff = Jw * N - Jw * (Jw - 1) / 2 - Jw + I0;
+        ln.wsl = seq;
     }
 
     // ---------------- stage B: B_h[r][l] on DMMA -> stage-C A fragments ----------------
+    // A-stationary: the fragments of row tile rt pass through a one-tile buffer (D layout ->
+    // A layout) into registers areg[rt][*], which stage C keeps for the whole group; the
+    // stage-B B operand (Abar fragments) and this lane's trial-side 1D values are loaded
+    // once per group
+    constexpr bool AST = pw_astat(S);
+    constexpr bool HOIST = AST && C::K == 1 && HXG_PW_BHOIST;
+    constexpr int NRTA = AST ? NRT : 1;
+    double areg[NRTA][NK];
+    if constexpr (!AST) areg[0][0] = 0.0;
+    constexpr int NGH = HOIST ? pp.ng : 1, LTH = HOIST ? LT : 1, LQH = HOIST ? LQ : 1;
+    double agr[NGH][LTH][LQH], tbr[NGH][LQH];
     __syncwarp();  // previous group's stage C has read sB
-#pragma unroll 1
-    for (int rt = 0; rt < NRT; ++rt) {
+    if constexpr (HOIST) {
+        const int j2 = j2lo + (g8 & (NJ2 - 1));
+#pragma unroll
+        for (int g = 0; g < pp.ng; ++g) {
+            const double *Tb = sT + (pp.g_fs[g] * KT + j2 + shb1) * LP;
+#pragma unroll
+            for (int ks = 0; ks < LQ; ++ks) {
+                tbr[g][ks] = Tb[ks * 4 + t4];
+#pragma unroll
+                for (int lt = 0; lt < LT; ++lt) agr[g][lt][ks] = sA[(g * LT + lt) * LQ * 32 + ks * 32 + lane];
+            }
+        }
+    } else {
+        agr[0][0][0] = tbr[0][0] = 0.0;
+    }
+    auto stage_b_tile = [&](int rt, double *sBt) {
         __syncwarp();  // converged for the DMMAs after the previous tile's divergent stores
         const int kk = rt / TPK, row = (rt - kk * TPK) * 8 + g8;  // row inside digit kk's block
         const int jj2 = row & (NJ2 - 1);
@@ -376,9 +440,14 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
 #pragma unroll
                 for (int ks = 0; ks < LQ; ++ks) {
                     const int m = ks * 4 + t4;
-                    const double av = rv ? Ta[m] * Tb[m] : 0.0;
+                    double av;
+                    if constexpr (HOIST) av = rv ? Ta[m] * tbr[g][ks] : 0.0;
+                    else av = rv ? Ta[m] * Tb[m] : 0.0;
 #pragma unroll
-                    for (int lt = 0; lt < LT; ++lt) dmma_8x8x4(d[lt][0], d[lt][1], av, Ag[(lt * LQ + ks) * 32]);
+                    for (int lt = 0; lt < LT; ++lt) {
+                        if constexpr (HOIST) dmma_8x8x4(d[lt][0], d[lt][1], av, agr[g][lt][ks]);
+                        else dmma_8x8x4(d[lt][0], d[lt][1], av, Ag[(lt * LQ + ks) * 32]);
+                    }
                 }
             }
             // D[row g8][l = 8 lt + 2 t4 + c] -> A fragment (rt, k / 4), lane g8 * 4 + k % 4
@@ -389,24 +458,25 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
                     const int l = lt * 8 + 2 * t4 + c;
                     if (l < L) {
                         const int k = h * L + l;
-                        sB[(rt * NKS + (k >> 2)) * 32 + g8 * 4 + (k & 3)] = d[lt][c];
+                        sBt[(k >> 2) * 32 + g8 * 4 + (k & 3)] = d[lt][c];
                     }
                 }
             __syncwarp();
         }
+    };
+    if constexpr (AST) {
+#pragma unroll
+        for (int rt = 0; rt < NRT; ++rt) {
+            stage_b_tile(rt, sB);
+#pragma unroll
+            for (int ks = 0; ks < NK; ++ks) areg[rt][ks] = sB[ks * 32 + lane];
+        }
+    } else {
+#pragma unroll 1
+        for (int rt = 0; rt < NRT; ++rt) stage_b_tile(rt, sB + rt * NKS * 32);
     }
     __syncwarp();
     // ---------------- stage C: P-form on DMMA, column tiles in j1 order ----------------
-    constexpr int NRTA = pw_astat(S) ? NRT : 1;
-    double areg[NRTA][NK];
-    if constexpr (pw_astat(S)) {
-#pragma unroll
-        for (int rt = 0; rt < NRT; ++rt)
-#pragma unroll
-            for (int ks = 0; ks < NK; ++ks) areg[rt][ks] = sB[(rt * NKS + ks) * 32 + lane];
-    } else {
-        areg[0][0] = 0.0;
-    }
     int jdone = 0;  // trial digits j1 < jdone have been written out
     constexpr int NST = NCT / CTW;  // full steps; an odd NCT ends with one single-tile step
 #pragma unroll 1
@@ -415,7 +485,13 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
         int jnext;
         if (st < NST) {
             pw_step<S, P, L, A, B, NJ2, NK, CTW>(sT, sB, sS, ct, seq, os, orr, ln, areg);
-            jnext = ct + CTW < NCT ? ((ct + CTW) * 8) / n1a : n1b;
+            if constexpr (pw_direct(S)) {
+                jnext = ct + CTW < NCT ? ((ct + CTW) * 8) / n1a : n1b;
+            } else {
+                jnext = ct + 1 < NCT ? ln.ej1 : n1b;
+                ln.ei1 += 8;
+                while (ln.ei1 >= n1a) { ln.ei1 -= n1a; ++ln.ej1; }
+            }
         } else {
             if constexpr (NCT % CTW != 0) pw_step<S, P, L, A, B, NJ2, NK, 1>(sT, sB, sS, ct, seq, os, orr, ln, areg);
             jnext = n1b;
@@ -426,9 +502,8 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
             __syncwarp();
             for (int j1 = jdone; j1 < jnext; ++j1) {
                 if (lane < NJ2) {
-                    const double *slot = sS + ((seq + j1) % NSLOT) * (RJ * SEG) + lane * SEG;
-                    const int J = offB + j1 + n1b * (j2lo + lane + n2b * j3);
-                    const int goff = J * N - J * (J - 1) / 2 - J + I0;
+                    const double *slot = sS + ln.wsl * (RJ * SEG) + lane * SEG;
+                    const int J = ln.wJ, goff = ln.wgoff;
                     const int cs = J > I0 ? J - I0 : 0;
                     const double *src = slot + ((epar + goff) & 1) + cs;
                     double *dst = outE + goff + cs;
@@ -441,6 +516,10 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
                     }
                     if (len & 1) __stcs(dst + len - 1, src[len - 1]);
                     if (len >= 2) bulk_s2g(dst, src, (len & ~1) * 8);
+                    // next trial digit: row J + 1 starts N - 1 - J entries further on
+                    ln.wgoff = goff + (N - 1) - J;
+                    ln.wJ = J + 1;
+                    ln.wsl = ln.wsl + 1 == NSLOT ? 0 : ln.wsl + 1;
                 }
                 bulk_commit();
             }
@@ -448,7 +527,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
             jdone = jnext;
         }
     }
-    if constexpr (!pw_direct(S)) seq += n1b;  // sequence numbers of completed trial digits
+    if constexpr (!pw_direct(S)) seq = (seq + n1b) % NSLOT;  // slot of the next group's first trial digit
 }
 
 template <int S, int P, int L, int A, int B>

@@ -172,7 +172,7 @@ __device__ __forceinline__ void bulk_s2g(double *gdst, const double *ssrc, int b
     const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
 #if HXG_BULK_HINT
     unsigned long long pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));  // not volatile: hoisted out of copy loops
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(gdst),
                  "r"(s), "r"(bytes), "l"(pol)
                  : "memory");
