@@ -74,6 +74,14 @@ __host__ __device__ constexpr bool pw_direct(int S) { return HXG_PW_WO < 0 ? (S 
 #ifndef HXG_PW_ASTAT
 #define HXG_PW_ASTAT -1
 #endif
+#ifndef HXG_PW_STSWZ
+#define HXG_PW_STSWZ 0  // staged write-out: swizzled store order (see pw_step)
+#endif
+// A-stationary groups: most stage-C A-fragment doubles a lane holds (row tiles x k-steps);
+// block pairs whose 8-digit groups need more run 4-digit (2-, 1-digit) groups
+#ifndef HXG_PW_AREG_MAX
+#define HXG_PW_AREG_MAX 50
+#endif
 #ifndef HXG_PW_BHOIST
 #define HXG_PW_BHOIST 1  // A-stationary groups: stage-B B fragments and trial-side 1D values in registers
 #endif
@@ -185,6 +193,27 @@ struct PWCfg {
     }
     static constexpr int NU = units();
 };
+
+__host__ __device__ constexpr int pw_rj_cap(int K, int n2a, int nk)
+{
+    int r = 1;
+    for (int q = 2; q <= 8; q *= 2)
+        if (K * ((q * n2a + 7) / 8) * nk <= HXG_PW_AREG_MAX) r = q;
+    return r;
+}
+
+template <int I>
+struct PWInt {
+    static constexpr int value = I;
+};
+template <int N, int I = 0, class F>
+__device__ __forceinline__ void pw_static_for(F &&f)
+{
+    if constexpr (I < N) {
+        f(PWInt<I>{});
+        pw_static_for<N, I + 1>(f);
+    }
+}
 
 struct PWArgs {
     const double *tables;
@@ -307,6 +336,10 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
     // newest one (NSLOT digits back) committed its copies >= NSLOT - 1 - JSPAN groups ago
     asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(NSLOT - 1 - C::JSPAN) : "memory");
     __syncwarp();
+    // store order o holds fragment column c = o ^ (t4 & 1): lanes of a quad then hit
+    // columns 0, 3, 4, 7 (then 1, 2, 5, 6) -- both bank parities in one store, so the
+    // even segment stride does not fold 32 lanes onto 8 of the 16 8-byte banks
+    const bool sw = HXG_PW_STSWZ && (t4 & 1);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
         const int j1 = ln.sj1[c], i1 = ln.si1[c];
@@ -314,7 +347,8 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
             double *base = sS + ln.ssl[c] * (RJ * SEG) + ln.rowoff0 + i1 + ((ln.pat >> (j1 & 3)) & 1);
 #pragma unroll
             for (int rt = 0; rt < NRT; ++rt)
-                if ((rt % TPK < TPK - 1 || lastv) && HXG_PW_SKIP_WO < 2) base[R::off(rt)] = d[0][rt][c];
+                if ((rt % TPK < TPK - 1 || lastv) && HXG_PW_SKIP_WO < 2)
+                    base[R::off(rt)] = sw ? d[0][rt][1 - c] : d[0][rt][c];
         }
         ln.si1[c] = i1 + 8;
         while (ln.si1[c] >= n1a) {
@@ -376,9 +410,10 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
         ln.bj1 = g8 / n1a;
         ln.bi1 = g8 % n1a;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            ln.sj1[c] = (2 * t4 + c) / n1a;
-            ln.si1[c] = (2 * t4 + c) % n1a;
+        for (int c = 0; c < 2; ++c) {  // store order c <-> fragment column c ^ (t4 & 1)
+            const int col = 2 * t4 + (HXG_PW_STSWZ ? (c ^ (t4 & 1)) : c);
+            ln.sj1[c] = col / n1a;
+            ln.si1[c] = col % n1a;
             ln.ssl[c] = (seq + ln.sj1[c]) % NSLOT;
         }
         ln.ej1 = 8 / n1a;
@@ -418,6 +453,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
         agr[0][0][0] = tbr[0][0] = 0.0;
     }
     auto stage_b_tile = [&](int rt, double *sBt) {
+        constexpr CPair pp = make_pair_plan(S, A, B);  // not captured: stays a compile-time constant
         __syncwarp();  // converged for the DMMAs after the previous tile's divergent stores
         const int kk = rt / TPK, row = (rt - kk * TPK) * 8 + g8;  // row inside digit kk's block
         const int jj2 = row & (NJ2 - 1);
@@ -465,12 +501,13 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
         }
     };
     if constexpr (AST) {
-#pragma unroll
-        for (int rt = 0; rt < NRT; ++rt) {
+        // forced unrolling (areg must be indexed statically to stay in registers)
+        pw_static_for<NRT>([&](auto rtc) {
+            constexpr int rt = decltype(rtc)::value;
             stage_b_tile(rt, sB);
 #pragma unroll
             for (int ks = 0; ks < NK; ++ks) areg[rt][ks] = sB[ks * 32 + lane];
-        }
+        });
     } else {
 #pragma unroll 1
         for (int rt = 0; rt < NRT; ++rt) stage_b_tile(rt, sB + rt * NKS * 32);
@@ -536,7 +573,7 @@ __device__ __forceinline__ void pw_unit(const double *sT, double *W, const doubl
 {
     using C = PWCfg<S, P, L>;
     constexpr CPair pp = make_pair_plan(S, A, B);
-    constexpr int LP = C::LP, L3 = C::L3, LQ = C::LQ, LT = C::LT, RJ = C::RJ;
+    constexpr int LP = C::LP, L3 = C::L3, LQ = C::LQ, LT = C::LT;
     const int kc = cmin(C::K, C::n(A, 2) - i3);  // test digits i3 .. i3 + kc - 1 of this unit
     constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1), n2b = C::n(B, 1);
     constexpr int sha0 = sh_of(S, A, 0), sha2 = sh_of(S, A, 2);
@@ -626,7 +663,9 @@ __device__ __forceinline__ void pw_unit(const double *sT, double *W, const doubl
     }
 
     const int I0 = offA + n1a * n2a * i3;
-    // trial digits j2 in groups of 8, 4, 2, 1 (largest first, at most RJ)
+    // trial digits j2 in groups of 8, 4, 2, 1 (largest first, at most RJ; A-stationary
+    // pairs also bound the fragment registers of a group)
+    constexpr int RJ = pw_astat(S) ? cmin(C::RJ, pw_rj_cap(C::K, n2a, NK)) : C::RJ;
     int j2lo = 0;
 #pragma unroll 1
     while (j2lo < n2b) {
