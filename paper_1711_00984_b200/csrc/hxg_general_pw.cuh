@@ -82,6 +82,9 @@ __host__ __device__ constexpr bool pw_direct(int S) { return HXG_PW_WO < 0 ? (S 
 #ifndef HXG_PW_AREG_MAX
 #define HXG_PW_AREG_MAX 50
 #endif
+#ifndef HXG_PW_NSG_MAX
+#define HXG_PW_NSG_MAX 0  // > 0: short groups re-divide the staging area into up to this many slots (measured: no gain)
+#endif
 #ifndef HXG_PW_BHOIST
 #define HXG_PW_BHOIST 1  // A-stationary groups: stage-B B fragments and trial-side 1D values in registers
 #endif
@@ -142,6 +145,15 @@ struct PWCfg {
     // writes plus one whose bulk copies may still be reading
     static constexpr int NSLOT = JSPAN + 2;
     static constexpr int NSLOT_SMEM = pw_direct(S) ? 0 : NSLOT;
+    // a group of nj2 < RJ trial digits divides the same staging area into more, smaller
+    // slots (nj2 segments each): short groups have short steps, and with NSLOT slots a
+    // step would wait for the smem reads of the bulk copies issued two steps earlier
+    __host__ __device__ static constexpr int nsg(int nj2, int rj)
+    {
+        return HXG_PW_NSG_MAX > 0 ? cmin(HXG_PW_NSG_MAX, (NSLOT * rj) / nj2) : NSLOT;
+    }
+    // segments per slot
+    __host__ __device__ static constexpr int slotrows(int nj2, int rj) { return HXG_PW_NSG_MAX > 0 ? nj2 : rj; }
     static constexpr int WARPS = PW_WARPS, THREADS = PW_THREADS;
     static constexpr int SEG = ((K * C12 + 2 + 1) / 2) * 2;  // staging segment stride (even, >= K C12 + 1)
     // per-warp shared memory (doubles) for groups of at most rj in {1, 2, 4, 8} trial digits
@@ -254,7 +266,25 @@ struct PWLane {
     int ej1, ei1;        // (j1, i1) of column (ct + 1) * 8: trial digits below ej1 are complete
     // bulk write-out (lanes < NJ2): packed row of the next trial digit to leave
     int wJ, wgoff, wsl;  // its row, offset of (row, column I0) in the element, staging slot
+    // copy of that digit, prepared ahead of the step's DMMAs (integer work in their shadow)
+    const double *bsrc;
+    double *bdst;
+    int blen;
 };
+
+// Source, destination and length of lane's segment of the next trial digit to leave
+// (alignment fix-ups are applied at issue time).
+template <int RJSEG, int SEG, int C12a>
+__device__ __forceinline__ void pw_bulk_prep(PWLane &ln, const double *sS, double *outE, int epar, int I0, int kc)
+{
+    const int lane = threadIdx.x & 31;
+    const double *slot = sS + ln.wsl * RJSEG + lane * SEG;
+    const int J = ln.wJ, goff = ln.wgoff;
+    const int cs = J > I0 ? J - I0 : 0;
+    ln.bsrc = slot + ((epar + goff) & 1) + cs;
+    ln.bdst = outE + goff + cs;
+    ln.blen = kc * C12a - cs;
+}
 
 // One stage-C step: CTW column tiles starting at column tile ct, all row tiles of the
 // group, then the staging stores of this lane's D fragments.
@@ -264,7 +294,7 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
                                         const double (&areg)[NRTA][NK])
 {
     using C = PWCfg<S, P, L>;
-    constexpr int LP = C::LP, NKS = C::NKS, SEG = C::SEG, NSLOT = C::NSLOT, RJ = C::RJ;
+    constexpr int LP = C::LP, NKS = C::NKS, SEG = C::SEG, NSLOT = C::nsg(NJ2, C::RJ), RJ = C::slotrows(NJ2, C::RJ);
     constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1), n1b = C::n(B, 0);
     constexpr int NCOL = n1b * n1a;
     using R = PWRows<NJ2, C::K, n1a, n2a>;
@@ -370,7 +400,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
     using C = PWCfg<S, P, L>;
     constexpr CPair pp = make_pair_plan(S, A, B);
     constexpr int LP = C::LP, N = C::N, LQ = C::LQ, LT = C::LT, NKS = C::NKS;
-    constexpr int SEG = C::SEG, NSLOT = C::NSLOT, RJ = C::RJ;
+    constexpr int SEG = C::SEG, NSLOT = C::nsg(NJ2, C::RJ), RJ = C::slotrows(NJ2, C::RJ);
     constexpr int n1a = C::n(A, 0), n2a = C::n(A, 1);
     constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1);
     constexpr int sha1 = sh_of(S, A, 1), shb1 = sh_of(S, B, 1);
@@ -380,11 +410,22 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
     using R = PWRows<NJ2, C::K, n1a, n2a>;
     constexpr int NRT = R::NRT, TPK = R::TPK;
     constexpr int CTW = C::ctw(A, B);
-    static_assert(NRT <= C::RTM && NJ2 <= RJ && 8 % NJ2 == 0, "group shape");
+    static_assert(NRT <= C::RTM && NJ2 <= C::RJ && 8 % NJ2 == 0, "group shape");
     const int lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
     const double *sA = W + C::W_A;
     double *sB = W + C::W_B, *sS = W + C::W_S;
 
+    // seq = (slot of the group's first trial digit) | (NJ2 of the staging layout) << 4; a group
+    // with another NJ2 re-divides the staging area, so every copy in flight must have read
+    // its slot first
+    if constexpr (!pw_direct(S) && HXG_PW_NSG_MAX > 0) {
+        if ((seq >> 4) != NJ2) {
+            bulk_wait_read();
+            __syncwarp();
+            seq = NJ2 << 4;
+        }
+    }
+    const int seq0 = seq & 15;
     // this lane's rows r = rt * 8 + g8 = i2 * NJ2 + jj2 all carry jj2 = g8 % NJ2
     PWLane ln;
     {
@@ -414,14 +455,14 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
             const int col = 2 * t4 + (HXG_PW_STSWZ ? (c ^ (t4 & 1)) : c);
             ln.sj1[c] = col / n1a;
             ln.si1[c] = col % n1a;
-            ln.ssl[c] = (seq + ln.sj1[c]) % NSLOT;
+            ln.ssl[c] = (seq0 + ln.sj1[c]) % NSLOT;
         }
         ln.ej1 = 8 / n1a;
         ln.ei1 = 8 % n1a;
         const int Jw = offB + n1b * (j2lo + lane + n2b * j3);  // lanes < NJ2 own trial digit jj2 = lane
         ln.wJ = Jw;
         ln.wgoff = Jw * N - Jw * (Jw - 1) / 2 - Jw + I0;
-        ln.wsl = seq;
+        ln.wsl = seq0;
     }
 
     // ---------------- stage B: B_h[r][l] on DMMA -> stage-C A fragments ----------------
@@ -520,6 +561,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
     for (int st = 0; st <= NST; ++st) {
         const int ct = st * CTW;
         int jnext;
+        if constexpr (!pw_direct(S)) pw_bulk_prep<RJ * SEG, SEG, C12a>(ln, sS, outE, epar, I0, kc);
         if (st < NST) {
             pw_step<S, P, L, A, B, NJ2, NK, CTW>(sT, sB, sS, ct, seq, os, orr, ln, areg);
             if constexpr (pw_direct(S)) {
@@ -538,13 +580,12 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
             fence_proxy_async();
             __syncwarp();
             for (int j1 = jdone; j1 < jnext; ++j1) {
+                if (j1 > jdone) pw_bulk_prep<RJ * SEG, SEG, C12a>(ln, sS, outE, epar, I0, kc);
                 if (lane < NJ2) {
-                    const double *slot = sS + ln.wsl * (RJ * SEG) + lane * SEG;
                     const int J = ln.wJ, goff = ln.wgoff;
-                    const int cs = J > I0 ? J - I0 : 0;
-                    const double *src = slot + ((epar + goff) & 1) + cs;
-                    double *dst = outE + goff + cs;
-                    int len = kc * C12a - cs;
+                    const double *src = ln.bsrc;
+                    double *dst = ln.bdst;
+                    int len = ln.blen;
                     if (reinterpret_cast<size_t>(dst) & 8) {
                         __stcs(dst, *src);
                         ++dst;
@@ -564,7 +605,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
             jdone = jnext;
         }
     }
-    if constexpr (!pw_direct(S)) seq = (seq + n1b) % NSLOT;  // slot of the next group's first trial digit
+    if constexpr (!pw_direct(S)) seq = ((seq0 + n1b) % NSLOT) | (HXG_PW_NSG_MAX > 0 ? NJ2 << 4 : 0);  // slot of the next group's first trial digit
 }
 
 template <int S, int P, int L, int A, int B>
@@ -670,6 +711,9 @@ __device__ __forceinline__ void pw_unit(const double *sT, double *W, const doubl
 #pragma unroll 1
     while (j2lo < n2b) {
         const int rem = n2b - j2lo;
+#ifdef HXG_PW_SKIP_REM  // timing experiment only (wrong results): drop the groups below RJ digits
+        if (rem < RJ) break;
+#endif
         if (RJ >= 8 && rem >= 8) {
             if constexpr (RJ >= 8) pw_group<S, P, L, A, B, 8>(sT, W, outE, epar, j3, I0, kc, j2lo, os, orr, seq);
             j2lo += 8;
