@@ -18,6 +18,9 @@
 namespace hxg {
 
 constexpr int AFF2_THREADS = 128;
+#ifndef HXG_AFF_FLAT
+#define HXG_AFF_FLAT 0  // 1: aff_rows deals (row, column chunk) items to the warps (measured 20-40 % slower: a warp streaming one contiguous row writes faster than warps interleaving chunks)
+#endif
 
 struct AffV2Args {
     const int *kind;
@@ -99,6 +102,40 @@ __device__ __forceinline__ void aff_rows(const double *smem, double *__restrict_
     const bool act = kq < KW;
     const int Kp = j2 + n2b * j3;
     const int K0 = (A == B) ? Kp : 0;
+#if HXG_AFF_FLAT
+    // (trial row j1, chunk of KW test columns K) items dealt round-robin to the warps: the
+    // rows of a group are n1b = 5..11, which does not divide over the CTA's warps (a row
+    // per warp left 1 of 4 warps busy in the last round at n1b = 9)
+    constexpr int NW = AFF2_THREADS / 32;
+    const int nch = (n2a * n3a - K0 + KW - 1) / KW;  // chunks per row (the same for every j1 of the group)
+    int j1 = 0, ch = warp;
+    while (ch >= nch) { ch -= nch; ++j1; }
+    while (j1 < n1b) {
+        double Fr[MAXH];
+#pragma unroll
+        for (int h = 0; h < MAXH; ++h)
+            Fr[h] = h < pp.nh ? sF[((2 * pp.h_fr[h] + pp.h_fs[h]) * KF + i1 + sha0) * KF + j1 + shb0] : 0.0;
+        const int J = offB + j1 + n1b * Kp;
+        double *rowp = outE + (J * N - J * (J - 1) / 2 - J);  // &G(J, 0)
+#pragma unroll 4
+        for (; ch < nch; ch += NW) {
+            const int K = K0 + kq + KW * ch;
+            if (act && K < n2a * n3a) {
+                const int I = offA + K * n1a + i1;
+                const double2 b01 = *reinterpret_cast<const double2 *>(sBs + K * 4);
+                double v = Fr[0] * b01.x;
+                if (pp.nh > 1) v = fma(Fr[1], b01.y, v);
+                if (pp.nh > 2) {
+                    const double2 b23 = *reinterpret_cast<const double2 *>(sBs + K * 4 + 2);
+                    v = fma(Fr[2], b23.x, v);
+                    if (pp.nh > 3) v = fma(Fr[3], b23.y, v);
+                }
+                if (I >= J) __stcs(rowp + I, v);
+            }
+        }
+        while (ch >= nch && j1 < n1b) { ch -= nch; ++j1; }
+    }
+#else
     for (int j1 = warp; j1 < n1b; j1 += AFF2_THREADS / 32) {
         double Fr[MAXH];
 #pragma unroll
@@ -122,6 +159,7 @@ __device__ __forceinline__ void aff_rows(const double *smem, double *__restrict_
             }
         }
     }
+#endif
 }
 
 // Bs_h[A][K] for one (test block A, trial block B) pair

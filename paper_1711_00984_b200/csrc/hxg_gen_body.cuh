@@ -105,9 +105,12 @@ int gen_launch_one(const V2Args &a, cudaStream_t st)
             b.split = a.E >= sms * C3::MINB ? 1 : (want + a.E - 1) / a.E;
             if (b.split > 16) b.split = 16;
             if (getenv("HXG_V3_SPLIT")) b.split = atoi(getenv("HXG_V3_SPLIT"));
-            // persistent CTAs (grid-stride over (element, part) items)
-            const long long items = (long long)a.E * b.split;
-            const int grid = (int)std::min<long long>(items, (long long)sms * C3::MINB * 2);
+            // persistent CTAs (grid-stride over (element, part) items), or one wave of
+            // CTAs with equal item ranges (HXG_V3_RANGE=1)
+            const char *rg = getenv("HXG_V3_RANGE");
+            b.range = (!C3::FUSED && b.split == 1 && rg && rg[0] == '1') ? 1 : 0;  // measured: no gain (H(curl) p6 -10 %)
+            const long long items = b.range ? (long long)a.E * C3::NU : (long long)a.E * b.split;
+            const int grid = (int)std::min<long long>(items, (long long)sms * C3::MINB * (b.range ? 1 : 2));
             k3<<<grid, V3_THREADS, C3::SMEM_BYTES, st>>>(b);
             return cudaGetLastError() == cudaSuccess ? 0 : -5;
         }

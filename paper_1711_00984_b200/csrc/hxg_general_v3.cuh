@@ -116,6 +116,7 @@ struct V3Args {
     long long P;
     int E;
     int split;  // CTAs per element
+    int range;  // 1: CTA c owns the contiguous (element, unit) items [c T / G, (c + 1) T / G), T = E * NU
     // fused low-order path (C::FUSED): geometry evaluated in the kernel
     const int *kind;
     const double *params, *coef, *wgrid;
@@ -630,7 +631,27 @@ __global__ void __launch_bounds__(V3_THREADS, (V3Cfg<S, P, L>::MINB))
 #ifndef HXG_V3_FLOW
 #define HXG_V3_FLOW 1
 #endif
-    if (HXG_V3_FLOW && !C::FUSED && args.split == 1) {
+    if (HXG_V3_FLOW && !C::FUSED && args.split == 1 && args.range) {
+        // one wave of CTAs, equal shares of the (element, unit) items down to one unit: no
+        // tail of CTAs that drew one element more than the others (1024-element batches
+        // are ~3.5 elements per resident CTA)
+        if (threadIdx.x == 0) s_next = 0;
+        __syncthreads();
+        const long long T = (long long)args.E * C::NU;
+        const long long lo = T * blockIdx.x / gridDim.x, hi = T * (blockIdx.x + 1) / gridDim.x;
+        for (;;) {
+            int u = 0;
+            if (lane == 0) u = atomicAdd(&s_next, 1);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            const long long item = lo + u;
+            if (item >= hi) break;
+            const int e = (int)(item / C::NU);
+            const double *M = args.metric + (long long)e * C::NF * C::L3;
+            double *__restrict__ outE = args.out + (long long)e * args.P;
+            const int epar = (int)((reinterpret_cast<size_t>(outE) >> 3) & 1);
+            v3_run_unit<S, P, L>((int)(item - (long long)e * C::NU), args, sT, W, M, outE, epar, buf, keep);
+        }
+    } else if (HXG_V3_FLOW && !C::FUSED && args.split == 1) {
         // one CTA counter over (element, unit) pairs: a warp that finds no unit left in
         // its element moves on to the CTA's next element instead of waiting at a barrier
         // for the element's last unit (8.6 % of the warp samples at H1 p5)
