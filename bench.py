@@ -335,11 +335,11 @@ class DeviceStep:
         self.out = torch.empty((E, self.P), dtype=torch.float64, device=dev)
         self.status = torch.zeros(E, dtype=torch.int32, device=dev)
         self.tab = self.eng.tables(self.L)
-        # p <= 3 runs one fused kernel (geometry in the contraction kernel): time the
+        # low orders (p <= hxg_fused_order_max()) run one kernel (geometry evaluated in the contraction kernel): time the
         # whole hxg_gram_batched call; otherwise time metric and contraction separately,
         # with a workspace holding the metric fields of the whole batch
         # (hxg_workspace_size is capped at one 512 MB launch chunk)
-        self.fused = wl.path == "general" and wl.p <= 3
+        self.fused = wl.path == "general" and wl.p <= self.lib.hxg_fused_order_max()
         ws = self.lib.hxg_workspace_size(self.sc, self.pc,
                                          *wl.orders, self.L, E)
         per = self.lib.hxg_workspace_size(self.sc, 0, *wl.orders, self.L, 1) if wl.path == "general" else 0

@@ -73,6 +73,11 @@ enum {
 
 /* library version, e.g. 100 for 0.1.0 */
 int hxg_version(void);
+
+/* Highest isotropic order p (rule L = p + 1) for which hxg_gram_batched(path = 0) runs as
+ * one kernel that evaluates the element geometry itself -- no hxg_metric_batched pass and
+ * no workspace.  hxg_metric_batched + hxg_contract_batched remain valid at every order. */
+int hxg_fused_order_max(void);
 const char *hxg_error_string(int code);
 
 /* spaces.py:67-80 -- number of basis functions N; <0 on bad arguments */

@@ -44,6 +44,7 @@ PATH_CODES = {"general": 0, "affine": 1, "extrusion": 2}
 # every symbol the header declares (checked by the CPU test suite)
 EXPORTED = (
     "hxg_version",
+    "hxg_fused_order_max",
     "hxg_error_string",
     "hxg_dim",
     "hxg_accumulations",
@@ -90,6 +91,7 @@ def lib():
         )
     L = ctypes.CDLL(LIB_PATH)
     L.hxg_version.restype = _i
+    L.hxg_fused_order_max.restype = _i
     L.hxg_error_string.argtypes = [_i]
     L.hxg_error_string.restype = ctypes.c_char_p
     L.hxg_dim.argtypes = [_i, _i, _i, _i]

@@ -380,6 +380,8 @@ extern "C" {
 
 int hxg_version(void) { return 100; }
 
+int hxg_fused_order_max(void) { return hxg::fused_order_max(); }
+
 const char *hxg_error_string(int code)
 {
     switch (code) {
@@ -472,7 +474,7 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
                           !(force_generic && force_generic[0] == '1');
     // general path, unfused orders: the specialized metric kernel writes the words whole
     const char *force_v2 = getenv("HXG_FORCE_V2");
-    const bool fused_gen = path == GENERAL && p1 == p2 && p2 == p3 && p1 <= 3 && L == p1 + 1 &&
+    const bool fused_gen = path == GENERAL && p1 == p2 && p2 == p3 && p1 <= fused_order_max() && L == p1 + 1 &&
                            !(force_generic && force_generic[0] == '1') && !(force_v2 && force_v2[0] == '1');
     const bool met_writes = path == GENERAL && !fused_gen && metric_v2_ok(space, L) &&
                             !ext_gather_route(path, p1, p2, p3, L);
@@ -620,7 +622,7 @@ int hxg_gram_batched(int space, int path, int p1, int p2, int p3, int L, int E, 
     // the contraction kernel, no metric pass / workspace)
     {
         const char *fg = getenv("HXG_FORCE_GENERIC"), *f2 = getenv("HXG_FORCE_V2");
-        if (p1 == p2 && p2 == p3 && p1 <= 3 && L == p1 + 1 && !(fg && fg[0] == '1') &&
+        if (p1 == p2 && p2 == p3 && p1 <= fused_order_max() && L == p1 + 1 && !(fg && fg[0] == '1') &&
             !(f2 && f2[0] == '1')) {
             V2Args a;
             a.tables = tables;

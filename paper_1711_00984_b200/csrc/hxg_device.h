@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 
 namespace hxg {
 
@@ -20,6 +21,15 @@ inline int sm_count()
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
     cache[dev].store(v, std::memory_order_relaxed);
     return v;
+}
+
+// Highest isotropic order served by a kernel that evaluates the element geometry itself
+// (no metric pass / workspace): the low-order slab kernel general_lo_kernel covers
+// p <= 4; HXG_LO=0 falls back to the fused warp-unit kernel (p <= 3).
+inline int fused_order_max()
+{
+    const char *v = getenv("HXG_LO");
+    return (v && v[0] == '0') ? 3 : 4;
 }
 
 }  // namespace hxg

@@ -12,6 +12,7 @@
 #include "hxg_general_v2.cuh"
 #include "hxg_general_v3.cuh"
 #include "hxg_general_pw.cuh"
+#include "hxg_general_lo.cuh"
 #include "hxg_metric.cuh"
 #include "hxg_v2_launch.h"
 
@@ -76,6 +77,31 @@ int gen_launch_one(const V2Args &a, cudaStream_t st)
             const int grid = (int)std::min<long long>(items, std::min<long long>(g, 1ll << 30));
             kp<<<grid, CP::THREADS, CP::SMEM_BYTES, st>>>(b);
             return cudaGetLastError() == cudaSuccess ? 0 : -5;
+        }
+    }
+    // low orders, fused call (metric == NULL): the slab kernel (hxg_general_lo.cuh)
+    if constexpr (P <= 4) {
+        using CL = LoCfg<S, P>;
+        if constexpr (CL::OK) {
+            if (a.metric == nullptr && fused_order_max() >= 4) {
+                auto kl = general_lo_kernel<S, P>;
+                if (cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, CL::SMEM_BYTES) != cudaSuccess)
+                    return -5;
+                LoArgs b;
+                b.tables = a.tables;
+                b.out = a.out;
+                b.P = a.P;
+                b.E = a.E;
+                b.kind = a.kind;
+                b.params = a.params;
+                b.coef = a.coef;
+                b.wgrid = a.wgrid;
+                b.status = a.status;
+                const long long passes = ((long long)a.E + CL::EB - 1) / CL::EB;
+                const int grid = (int)std::min<long long>(passes, (long long)sm_count() * CL::MINB * 4);
+                kl<<<grid, LO_THREADS, CL::SMEM_BYTES, st>>>(b);
+                return cudaGetLastError() == cudaSuccess ? 0 : -5;
+            }
         }
     }
     using C3 = V3Cfg<S, P, P + 1>;
