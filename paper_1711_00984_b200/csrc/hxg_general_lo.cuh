@@ -34,6 +34,12 @@ namespace hxg {
 #define HXG_LO_THREADS 256
 #endif
 constexpr int LO_THREADS = HXG_LO_THREADS;
+#ifndef HXG_LO_BUDGET_KB
+#define HXG_LO_BUDGET_KB 100  // shared memory per CTA (2 CTAs per SM)
+#endif
+#ifndef HXG_LO_EBMAX
+#define HXG_LO_EBMAX 16  // most elements per CTA pass
+#endif
 
 template <int S, int P>
 struct LoCfg {
@@ -74,42 +80,50 @@ struct LoCfg {
         for (int b = 0; b < NB; ++b) m = cmax(m, aoff(NB, b));
         return m;
     }
-    static constexpr int A_TOT = amax();
-    // slab image: rows J0 .. J0 + R - 1 of the packed triangle, R = n1b n2b
-    __host__ __device__ static constexpr int imgmax()
+    static constexpr int A_TOT1 = amax();  // Abar of one slab
+    // image of nj consecutive slabs of a block: rows J0 .. J0 + nj R - 1 of the packed triangle
+    __host__ __device__ static constexpr int imgmax(int nj)
     {
         int m = 0;
         for (int b = 0; b < NB; ++b) {
-            const int R = n(b, 0) * n(b, 1), J0 = off(b);
+            const int R = n(b, 0) * n(b, 1) * cmin(nj, n(b, 2)), J0 = off(b);
             m = cmax(m, R * N - (R * J0 + R * (R - 1) / 2));
         }
-        return m;
+        return (m + 1) & ~1;
     }
-    static constexpr int IMG = (imgmax() + 1) & ~1;
-    // items of a slab: (a, i3, i2, j2)
-    __host__ __device__ static constexpr int items(int b)
-    {
-        int m = 0;
-        for (int a = b; a < NB; ++a) m += n(a, 2) * n(a, 1) * n(b, 1);
-        return m;
-    }
-    __host__ __device__ static constexpr int itemsmax()
-    {
-        int m = 0;
-        for (int b = 0; b < NB; ++b) m = cmax(m, items(b));
-        return m;
-    }
-    static constexpr int SLOT = ((NF * L3 + 1) & ~1) + A_TOT + IMG;  // doubles per element slot (parts even)
+    __host__ __device__ static constexpr int n3max() { return cmax(n(0, 2), NB > 1 ? cmax(n(1, 2), n(2, 2)) : 0); }
+    __host__ __device__ static constexpr int slot(int nj) { return ((NF * L3 + 1) & ~1) + nj * A_TOT1 + imgmax(nj); }
     static constexpr int COMMON = 2 * KT * LP + U_TOT;
-    // elements per CTA pass: fill the CTA with slab items, within ~100 KB
-    __host__ __device__ static constexpr int pick_eb()
+    static constexpr int BUDGET = (HXG_LO_BUDGET_KB * 1024) / 8;  // doubles per CTA
+    __host__ __device__ static constexpr int eb_of(int nj) { return cmin(HXG_LO_EBMAX, (BUDGET - COMMON) / slot(nj)); }
+    // slabs per pass: the most (slabs x elements) in flight between two barriers
+    __host__ __device__ static constexpr int pick_nj()
     {
+        int best = 1, score = 0;
+        for (int nj = 1; nj <= n3max(); ++nj) {
+            // average slabs per pass (x 60, exact for n3 <= 5) times the elements of a pass
+            const int passes = (n3max() + nj - 1) / nj;
+            const int sc = eb_of(nj) * (60 * n3max() / passes);
+            if (sc >= score && eb_of(nj) >= 1) { score = sc; best = nj; }
+        }
+        return best;
+    }
+    // single-block spaces (H1, L2): one slab per pass and as many elements as fill the CTA
+    // with slab items (measured: H1 p3 60 vs 52 M el/s for whole-element passes -- idle
+    // warps of a short slab cost nothing while the SM's other CTA runs)
+    __host__ __device__ static constexpr int eb_single()
+    {
+        const int items = n(0, 2) * n(0, 1) * n(0, 1);
         int eb = 1;
-        for (int q = 2; q <= 8; q *= 2)
-            if (q * itemsmax() <= LO_THREADS + LO_THREADS / 4 && (COMMON + q * SLOT) * 8 <= 100 * 1024) eb = q;
+        for (int q = 2; q <= HXG_LO_EBMAX; q *= 2)
+            if (q * items <= LO_THREADS + LO_THREADS / 4 && q <= eb_of(1)) eb = q;
         return eb;
     }
-    static constexpr int EB = pick_eb();
+    static constexpr int NJ3 = NB == 1 ? 1 : pick_nj();
+    static constexpr int EB = NB == 1 ? eb_single() : cmax(1, eb_of(NJ3));
+    static constexpr int A_TOT = NJ3 * A_TOT1;
+    static constexpr int IMG = imgmax(NJ3);
+    static constexpr int SLOT = slot(NJ3);  // doubles per element slot (parts even)
     static constexpr int TPE = LO_THREADS / EB;
     static constexpr int SMEM_BYTES = (COMMON + EB * SLOT) * 8;
     static constexpr bool OK = SMEM_BYTES <= 200 * 1024 && P >= 1 && P <= 5;
@@ -169,10 +183,10 @@ __device__ __forceinline__ void lo_stage_a(const double *sT, const double *sM, d
     }
 }
 
-// stages B and C of one block pair: one item (i3, i2, j2) per thread pass
+// stages B and C of one item (i3, i2, j2) of block pair (A, B) in the slab (b, j3)
 template <int S, int P, int A, int B>
-__device__ __forceinline__ void lo_stage_bc(const double *sT, const double *sU, const double *sA, double *sImg,
-                                            int j3, int it0, int stride, int &base)
+__device__ __forceinline__ void lo_item(const double *sT, const double *sU, const double *sA, double *sImg,
+                                        int J0, int j3, int i3, int i2, int j2)
 {
     using C = LoCfg<S, P>;
     constexpr CPair pp = make_pair_plan(S, A, B);
@@ -181,16 +195,10 @@ __device__ __forceinline__ void lo_stage_bc(const double *sT, const double *sU, 
     constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1);
     constexpr int sha1 = sh_of(S, A, 1), shb1 = sh_of(S, B, 1);
     constexpr int offA = C::off(A), offB = C::off(B);
-    constexpr int NIT = n3a * n2a * n2b;
     const double *U = sU + C::uoff(A, B);
     const double *Ab = sA + C::aoff(A, B);
-    const int J0 = offB + n1b * n2b * j3;  // first packed row of the slab
-    // items of this pair occupy [base, base + NIT) of the slab's item list
-    int gfirst = it0;  // this thread's first item index >= base (items it0, it0 + stride, ...)
-    if (gfirst < base) gfirst += ((base - gfirst + stride - 1) / stride) * stride;
-    for (int it = gfirst - base; it < NIT; it += stride) {
-        const int i2 = it % n2a, r = it / n2a, j2 = r % n2b, i3 = r / n2b;
-        if (A == B && (i3 < j3 || (i3 == j3 && i2 < j2))) continue;  // wholly below the diagonal
+    // J0: first packed row of the pass's image
+    {
         // ---- stage B: B_h[l] in registers
         double Bh[pp.nh][L];
 #pragma unroll
@@ -265,33 +273,93 @@ __device__ __forceinline__ void lo_stage_bc(const double *sT, const double *sU, 
             }
         }
     }
-    base += NIT;
 }
 
+// One pass: the slabs j3lo .. j3lo + nj - 1 of trial block B (a contiguous range of packed rows)
 template <int S, int P, int B>
-__device__ __forceinline__ void lo_slab(const double *sT, const double *sU, const double *sM, double *sA,
-                                        double *sImg, double *__restrict__ outE, int j3, int tin, bool live)
+__device__ __forceinline__ void lo_pass(const double *sT, const double *sU, const double *sM, double *sA0,
+                                        double *sImg0, double *__restrict__ outE, int j3lo, int nj, int slot,
+                                        int tin, bool live, int nlive)
 {
     using C = LoCfg<S, P>;
+    // slot-0 pointers sA0 / sImg0: stage A and the write-out work on this thread's own
+    // slot, the items of stage BC on any live slot
+    double *sA = sA0 + slot * C::SLOT, *sImg = sImg0 + slot * C::SLOT;
     constexpr int N = C::N;
-    constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1), offB = C::off(B);
+    constexpr int n1b = C::n(B, 0), n2b = C::n(B, 1), n3b = C::n(B, 2), offB = C::off(B);
+    constexpr int R = n1b * n2b;
+    const int J0 = offB + R * j3lo;
     if (live) {
-        lo_stage_a<S, P, B, B>(sT, sM, sA, j3, tin);
-        if constexpr (C::NB > 1 && B <= 1) lo_stage_a<S, P, B + 1 < 3 ? B + 1 : 2, B>(sT, sM, sA, j3, tin);
-        if constexpr (C::NB > 1 && B == 0) lo_stage_a<S, P, 2, B>(sT, sM, sA, j3, tin);
+        for (int sj = 0; sj < nj; ++sj) {
+            lo_stage_a<S, P, B, B>(sT, sM, sA + sj * C::A_TOT1, j3lo + sj, tin);
+            if constexpr (C::NB > 1 && B <= 1)
+                lo_stage_a<S, P, B + 1 < 3 ? B + 1 : 2, B>(sT, sM, sA + sj * C::A_TOT1, j3lo + sj, tin);
+            if constexpr (C::NB > 1 && B == 0) lo_stage_a<S, P, 2, B>(sT, sM, sA + sj * C::A_TOT1, j3lo + sj, tin);
+        }
     }
-    __syncthreads();  // Abar ready; the previous slab's image has been written out
-    if (live) {
-        int base = 0;
-        lo_stage_bc<S, P, B, B>(sT, sU, sA, sImg, j3, tin, C::TPE, base);
-        if constexpr (C::NB > 1 && B <= 1) lo_stage_bc<S, P, B + 1 < 3 ? B + 1 : 2, B>(sT, sU, sA, sImg, j3, tin, C::TPE, base);
-        if constexpr (C::NB > 1 && B == 0) lo_stage_bc<S, P, 2, B>(sT, sU, sA, sImg, j3, tin, C::TPE, base);
+    __syncthreads();  // Abar ready; the previous pass's image has been written out
+    {
+        // items of the pass, without those wholly below the diagonal, dealt to the whole CTA
+        // across its element slots; per slab: diagonal pair (i3 = j3: i2 >= j2; i3 > j3: all),
+        // then the pairs a > b
+        constexpr int n2sq = n2b * n2b, ntri = n2b * (n2b + 1) / 2;
+        constexpr int A1 = B + 1 < 3 ? B + 1 : 2;
+        constexpr int NIT1 = (C::NB > 1 && B <= 1) ? C::n(A1, 2) * C::n(A1, 1) * n2b : 0;
+        constexpr int NIT2 = (C::NB > 1 && B == 0) ? C::n(2, 2) * C::n(2, 1) * n2b : 0;
+        // slab j3 holds tot(j3) = ntri + (n3b - 1 - j3) n2sq + NIT1 + NIT2 items
+        int total = 0;
+        for (int sj = 0; sj < nj; ++sj) total += ntri + (n3b - 1 - (j3lo + sj)) * n2sq + NIT1 + NIT2;
+        for (int q = threadIdx.x; q < C::EB * total; q += LO_THREADS) {
+            const int sl = q / total;
+            int it = q - sl * total;
+            if (sl >= nlive) break;
+            int sj = 0, j3 = j3lo;
+            for (;;) {
+                const int t = ntri + (n3b - 1 - j3) * n2sq + NIT1 + NIT2;
+                if (it < t) break;
+                it -= t;
+                ++sj;
+                ++j3;
+            }
+            const double *sAq = sA0 + sl * C::SLOT + sj * C::A_TOT1;
+            double *sImgq = sImg0 + sl * C::SLOT;
+            const int nd = ntri + (n3b - 1 - j3) * n2sq;
+            if (it < nd) {
+                int i3, i2, j2;
+                if (it < ntri) {
+                    i3 = j3;
+                    j2 = 0;
+                    while (it >= n2b - j2) { it -= n2b - j2; ++j2; }
+                    i2 = j2 + it;
+                } else {
+                    it -= ntri;
+                    i3 = j3 + 1 + it / n2sq;
+                    it -= (i3 - j3 - 1) * n2sq;
+                    j2 = it / n2b;
+                    i2 = it - j2 * n2b;
+                }
+                lo_item<S, P, B, B>(sT, sU, sAq, sImgq, J0, j3, i3, i2, j2);
+            } else if (it < nd + NIT1) {
+                if constexpr (NIT1 > 0) {
+                    it -= nd;
+                    constexpr int n2a = C::n(A1, 1);
+                    const int i2 = it % n2a, r = it / n2a, j2 = r % n2b, i3 = r / n2b;
+                    lo_item<S, P, A1, B>(sT, sU, sAq, sImgq, J0, j3, i3, i2, j2);
+                }
+            } else {
+                if constexpr (NIT2 > 0) {
+                    it -= nd + NIT1;
+                    constexpr int n2a = C::n(2, 1);
+                    const int i2 = it % n2a, r = it / n2a, j2 = r % n2b, i3 = r / n2b;
+                    lo_item<S, P, 2, B>(sT, sU, sAq, sImgq, J0, j3, i3, i2, j2);
+                }
+            }
+        }
     }
     __syncthreads();  // image complete
     if (live) {
-        constexpr int R = n1b * n2b;
-        const int J0 = offB + R * j3;
-        const int len = R * N - (R * J0 + R * (R - 1) / 2);
+        const int Rp = R * nj;
+        const int len = Rp * N - (Rp * J0 + Rp * (Rp - 1) / 2);
         double *dst = outE + ((long long)J0 * N - (long long)J0 * (J0 - 1) / 2);
         for (int k = tin; k < len; k += C::TPE) __stcs(dst + k, sImg[k]);
     }
@@ -339,11 +407,12 @@ __global__ void __launch_bounds__(LO_THREADS, (LoCfg<S, P>::MINB)) general_lo_ke
     }
     const int slot = tid / C::TPE, tin = tid - slot * C::TPE;
     double *sM = smem + C::COMMON + slot * C::SLOT;  // [NF][L3]
-    double *sA = sM + ((C::NF * L3 + 1) & ~1);
-    double *sImg = sA + C::A_TOT;
+    double *sA0 = smem + C::COMMON + ((C::NF * L3 + 1) & ~1);  // slot 0: Abar, then the slab image
+    double *sImg0 = sA0 + C::A_TOT;
     for (long long e0 = (long long)blockIdx.x * C::EB; e0 < args.E; e0 += (long long)gridDim.x * C::EB) {
         const long long e = e0 + slot;
-        const bool live = e < args.E;
+        const bool live = slot < C::EB && e < args.E;  // (threads beyond EB * TPE only deal items)
+        const int nlive = (int)(args.E - e0 < C::EB ? args.E - e0 : C::EB);  // live slots of this pass
         __syncthreads();  // U tables (first pass); previous pass done with sM
         if (live) {
             const double *par = args.params + 24LL * e;
@@ -365,10 +434,13 @@ __global__ void __launch_bounds__(LO_THREADS, (LoCfg<S, P>::MINB)) general_lo_ke
         }
         __syncthreads();
         double *__restrict__ outE = args.out + (live ? e : 0) * args.P;
-        for (int j3 = 0; j3 < C::n(0, 2); ++j3) lo_slab<S, P, 0>(sT, sU, sM, sA, sImg, outE, j3, tin, live);
+        for (int j3 = 0; j3 < C::n(0, 2); j3 += C::NJ3)
+            lo_pass<S, P, 0>(sT, sU, sM, sA0, sImg0, outE, j3, cmin(C::NJ3, C::n(0, 2) - j3), slot, tin, live, nlive);
         if constexpr (NB > 1) {
-            for (int j3 = 0; j3 < C::n(1, 2); ++j3) lo_slab<S, P, 1>(sT, sU, sM, sA, sImg, outE, j3, tin, live);
-            for (int j3 = 0; j3 < C::n(2, 2); ++j3) lo_slab<S, P, 2>(sT, sU, sM, sA, sImg, outE, j3, tin, live);
+            for (int j3 = 0; j3 < C::n(1, 2); j3 += C::NJ3)
+                lo_pass<S, P, 1>(sT, sU, sM, sA0, sImg0, outE, j3, cmin(C::NJ3, C::n(1, 2) - j3), slot, tin, live, nlive);
+            for (int j3 = 0; j3 < C::n(2, 2); j3 += C::NJ3)
+                lo_pass<S, P, 2>(sT, sU, sM, sA0, sImg0, outE, j3, cmin(C::NJ3, C::n(2, 2) - j3), slot, tin, live, nlive);
         }
     }
 }
