@@ -31,11 +31,14 @@
 namespace hxg {
 
 #ifndef HXG_LO_THREADS
-#define HXG_LO_THREADS 256
+#define HXG_LO_THREADS 128
 #endif
 constexpr int LO_THREADS = HXG_LO_THREADS;
 #ifndef HXG_LO_BUDGET_KB
-#define HXG_LO_BUDGET_KB 100  // shared memory per CTA (2 CTAs per SM)
+#define HXG_LO_BUDGET_KB 50  // shared memory per CTA (4 CTAs per SM: more barrier domains per SM measured +3-14 % over 2 x 256 threads)
+#endif
+#ifndef HXG_LO_MAXB
+#define HXG_LO_MAXB 4  // CTAs per SM (register budget 65536 / (MAXB * THREADS))
 #endif
 #ifndef HXG_LO_EBMAX
 #define HXG_LO_EBMAX 16  // most elements per CTA pass
@@ -127,7 +130,7 @@ struct LoCfg {
     static constexpr int TPE = LO_THREADS / EB;
     static constexpr int SMEM_BYTES = (COMMON + EB * SLOT) * 8;
     static constexpr bool OK = SMEM_BYTES <= 200 * 1024 && P >= 1 && P <= 5;
-    static constexpr int MINB = cmax(1, cmin(2, (227 * 1024) / (SMEM_BYTES + 1024)));
+    static constexpr int MINB = cmax(1, cmin(HXG_LO_MAXB, (227 * 1024) / (SMEM_BYTES + 1024)));
 };
 
 template <int I>
