@@ -78,6 +78,11 @@ struct ExtCfg {
     }
 };
 
+template <int I>
+struct ExtInt {
+    static constexpr int value = I;
+};
+
 // stage A for test block A of the (A, B) pair: Abar[A][i3][g][m]
 // (LC: the rule order as a compile-time constant, 0 = runtime L)
 template <int S, int P, int LC, int A, int B>
@@ -91,6 +96,49 @@ __device__ __forceinline__ void ext_stage_a(double *smem, int Lr, int j3)
     const double *sT = smem + C::OFF_T, *sM = smem + C::OFF_M;
     double *sAb = smem + C::off_abar(L) + (size_t)A * N3 * NG * L;
     const int LL = L * L;
+    if constexpr (LC >= 1 && LC <= 8) {
+    // a thread owns (i3, m) and every GC-th term group; groups and terms are compile-time
+    // (with a runtime group index every thread ran all nt terms predicated: 17 % of the
+    // H1 p6 kernel's warp samples)
+    constexpr int GC = pp.ng >= 6 ? 3 : (pp.ng >= 2 ? 2 : 1);
+    for (int idx = threadIdx.x; idx < n3a * L * GC; idx += AFF2_THREADS) {
+        const int m = idx % L, q = idx / L, i3 = q % n3a, c = q / n3a;
+        // xi3 1D products of the four function-code pairs
+        double w3[2][2][LC ? LC : LT];
+#pragma unroll
+        for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+            for (int fs = 0; fs < 2; ++fs)
+#pragma unroll
+                for (int nn = 0; nn < (LC ? LC : LT); ++nn)
+                    w3[fr][fs][nn] = (LC || nn < L) ? sT[(fr * KT + i3 + sa2) * LT + nn] * sT[(fs * KT + j3 + sb2) * LT + nn] : 0.0;
+        auto run = [&](auto cc) {
+            constexpr int CC = decltype(cc)::value;
+            constexpr CPair pq = make_pair_plan(S, A, B);  // not captured: stays a compile-time constant
+#pragma unroll
+            for (int g = 0; g < pq.ng; ++g) {
+                if (g % GC != CC) continue;
+                double acc = 0.0;
+#pragma unroll
+                for (int t = 0; t < pq.nt; ++t) {
+                    if (pq.t_g[t] != g) continue;
+                    const double *Mt = sM + pq.t_field[t] * LL + m * L;
+                    double s = 0.0;
+#pragma unroll
+                    for (int nn = 0; nn < (LC ? LC : LT); ++nn)
+                        if (LC || nn < L) s = fma(Mt[nn], w3[pq.t_fr[t]][pq.t_fs[t]][nn], s);
+                    acc += pq.t_sign[t] > 0 ? s : -s;
+                }
+                sAb[(i3 * NG + g) * L + m] = acc;
+            }
+        };
+        if (c == 0) run(ExtInt<0>{});
+        if constexpr (GC > 1) if (c == 1) run(ExtInt<1>{});
+        if constexpr (GC > 2) if (c == 2) run(ExtInt<2>{});
+    }
+    } else {
+    // long rules (L > 8: the four 1D product vectors would cost more registers than they
+    // save; measured -20 % at p = 10) and runtime L: one (i3, g, m) entry per thread
     for (int idx = threadIdx.x; idx < n3a * pp.ng * L; idx += AFF2_THREADS) {
         const int m = idx % L, q = idx / L, g = q % pp.ng, i3 = q / pp.ng;
         double acc = 0.0;
@@ -107,6 +155,7 @@ __device__ __forceinline__ void ext_stage_a(double *smem, int Lr, int j3)
             acc += pp.t_sign[t] > 0 ? s : -s;
         }
         sAb[(i3 * NG + g) * L + m] = acc;
+    }
     }
 }
 
