@@ -455,39 +455,27 @@ __device__ AcBlock ac_block(int b, int pr, double omega)
 // shared memory (sOut).  The finished block is written once to each requested output:
 // its Bre or Bim part, zeros to the other part (the reference never writes those
 // blocks), and the four positions of the real block form B2 = [[Bre, -Bim], [Bim, Bre]].
-template <int P0C>  // trial order as a compile-time constant (0: runtime p0_arg)
-__global__ void __launch_bounds__(256) acoustics_block_kernel(int p0_arg, int pr, int L, double omega, int c3,
-                                                             const double *__restrict__ tab,
-                                                             const double *__restrict__ F,
-                                                             double *__restrict__ Bre,
-                                                             double *__restrict__ Bim,
-                                                             double *__restrict__ B2)
+// Slab loop of acoustics_block_kernel.  QC (= p_r + 1 = L), N2C (= n2) and CC (= the slab's
+// test digits i3, the whole extent n3) are compile-time when > 0: the index arithmetic of
+// stages A and B (divisions by c p0, n2 p0 c p0, ...) then folds to constants -- with
+// runtime divisors the kernel spent 60 % of its instructions on integer arithmetic
+// (profiles/prof_dpg_acoustics_r01_summary.txt: IMAD 24 %, ISETP 11 %, DFMA 2 %).
+template <int P0C, int QC, int N2C, int CC>
+__device__ __forceinline__ void ac_slabs(int p0_arg, int pr_arg, int L_arg, int c3_arg, int e, const AcBlock &B,
+                                         const double *sU, const double *sNu, const double *sW, double *sA,
+                                         double *sBt, double *sOut, const double *__restrict__ F,
+                                         double *__restrict__ Bre, double *__restrict__ Bim,
+                                         double *__restrict__ B2)
 {
     const int p0 = P0C > 0 ? P0C : p0_arg;
-    extern __shared__ double sm[];
-    const int b = blockIdx.x % 16, e = blockIdx.x / 16;  // 1D grid: E may exceed 65535
-    const AcBlock B = ac_block(b, pr, omega);
+    const int pr = QC > 0 ? QC - 1 : pr_arg;
+    const int L = QC > 0 ? QC : L_arg;
     const int q = pr + 1, mw = q * q * q, mv = 3 * q * pr * pr, m = mw + mv;
     const int ny = p0 * p0 * p0, n = 4 * ny;
     const int L3 = L * L * L;
-    const int sh0 = B.t[0].sh[0], sh1 = B.t[0].sh[1], sh2 = B.t[0].sh[2];  // shared by a block's terms
-    const int n1 = q - sh0, n2 = q - sh1, n3 = q - sh2;
-    // shared: 1D tables u[f][k][l] (f: chi, chi'), nu[k][l], w[l]; stage buffers for c3 digits i3
-    double *sU = sm;                         // [2][q + 1][L]
-    double *sNu = sU + 2 * (q + 1) * L;      // [p0][L]
-    double *sW = sNu + p0 * L;               // [L]
-    double *sA = sW + L;                     // [L][L][c3][p0]
-    double *sBt = sA + L * L * c3 * p0;      // [L][n2][p0][c3][p0]
-    double *sOut = sBt + L * n2 * p0 * c3 * p0;  // [n1 n2 c3][ny]
-    for (int i = threadIdx.x; i < 2 * (q + 1) * L; i += blockDim.x) {
-        const int f = i / ((q + 1) * L), r = i - f * (q + 1) * L, k = r / L, l = r - k * L;
-        sU[i] = tab[TAB_T + (f * KT + k) * LT + l];
-    }
-    for (int i = threadIdx.x; i < p0 * L; i += blockDim.x) {
-        const int k = i / L, l = i - k * L;
-        sNu[i] = tab[TAB_T + (1 * KT + k + 1) * LT + l];  // nu_k = chi'_{k+1}
-    }
-    for (int i = threadIdx.x; i < L; i += blockDim.x) sW[i] = tab[TAB_WTS + i];
+    const int sh0 = B.t[0].sh[0], sh1 = B.t[0].sh[1], sh2 = B.t[0].sh[2];
+    const int n1 = q - sh0, n2 = N2C > 0 ? N2C : q - sh1, n3 = CC > 0 ? CC : q - sh2;
+    const int c3 = CC > 0 ? CC : c3_arg;
     const double *Fe = F + (long long)e * AC_NF * L3;
     // stages A and B are separable in the test digit i3: slabs of c3 digits, no recomputation
     for (int i30 = 0; i30 < n3; i30 += c3) {
@@ -575,6 +563,52 @@ __global__ void __launch_bounds__(256) acoustics_block_kernel(int p0_arg, int pr
             }
         }
     }
+}
+
+template <int P0C, int DP>  // trial order and p_r - p0 as compile-time constants (0: runtime)
+__global__ void __launch_bounds__(256) acoustics_block_kernel(int p0_arg, int pr, int L, double omega, int c3,
+                                                             const double *__restrict__ tab,
+                                                             const double *__restrict__ F,
+                                                             double *__restrict__ Bre,
+                                                             double *__restrict__ Bim,
+                                                             double *__restrict__ B2)
+{
+    const int p0 = P0C > 0 ? P0C : p0_arg;
+    extern __shared__ double sm[];
+    const int b = blockIdx.x % 16, e = blockIdx.x / 16;  // 1D grid: E may exceed 65535
+    const AcBlock B = ac_block(b, pr, omega);
+    const int q = pr + 1, mw = q * q * q, mv = 3 * q * pr * pr, m = mw + mv;
+    const int ny = p0 * p0 * p0, n = 4 * ny;
+    const int L3 = L * L * L;
+    const int sh0 = B.t[0].sh[0], sh1 = B.t[0].sh[1], sh2 = B.t[0].sh[2];  // shared by a block's terms
+    const int n1 = q - sh0, n2 = q - sh1, n3 = q - sh2;
+    // shared: 1D tables u[f][k][l] (f: chi, chi'), nu[k][l], w[l]; stage buffers for c3 digits i3
+    double *sU = sm;                         // [2][q + 1][L]
+    double *sNu = sU + 2 * (q + 1) * L;      // [p0][L]
+    double *sW = sNu + p0 * L;               // [L]
+    double *sA = sW + L;                     // [L][L][c3][p0]
+    double *sBt = sA + L * L * c3 * p0;      // [L][n2][p0][c3][p0]
+    double *sOut = sBt + L * n2 * p0 * c3 * p0;  // [n1 n2 c3][ny]
+    for (int i = threadIdx.x; i < 2 * (q + 1) * L; i += blockDim.x) {
+        const int f = i / ((q + 1) * L), r = i - f * (q + 1) * L, k = r / L, l = r - k * L;
+        sU[i] = tab[TAB_T + (f * KT + k) * LT + l];
+    }
+    for (int i = threadIdx.x; i < p0 * L; i += blockDim.x) {
+        const int k = i / L, l = i - k * L;
+        sNu[i] = tab[TAB_T + (1 * KT + k + 1) * LT + l];  // nu_k = chi'_{k+1}
+    }
+    for (int i = threadIdx.x; i < L; i += blockDim.x) sW[i] = tab[TAB_WTS + i];
+    if constexpr (P0C > 0 && DP > 0) {
+        constexpr int Q = P0C + DP + 1;
+        if (pr == Q - 1 && L == Q && c3 == Q) {  // default rule, whole-extent slabs
+            if (sh1 == 0 && sh2 == 0) ac_slabs<P0C, Q, Q, Q>(p0, pr, L, c3, e, B, sU, sNu, sW, sA, sBt, sOut, F, Bre, Bim, B2);
+            else if (sh1 == 0) ac_slabs<P0C, Q, Q, Q - 1>(p0, pr, L, c3, e, B, sU, sNu, sW, sA, sBt, sOut, F, Bre, Bim, B2);
+            else if (sh2 == 0) ac_slabs<P0C, Q, Q - 1, Q>(p0, pr, L, c3, e, B, sU, sNu, sW, sA, sBt, sOut, F, Bre, Bim, B2);
+            else ac_slabs<P0C, Q, Q - 1, Q - 1>(p0, pr, L, c3, e, B, sU, sNu, sW, sA, sBt, sOut, F, Bre, Bim, B2);
+            return;
+        }
+    }
+    ac_slabs<P0C, 0, 0, 0>(p0, pr, L, c3, e, B, sU, sNu, sW, sA, sBt, sOut, F, Bre, Bim, B2);
 }
 
 // dpg.py:285-302: real part of the load over the stacked test space,
@@ -722,14 +756,18 @@ int hxg_acoustics_batched(int p0, int pr, double omega, int L, int E, const int 
     if (status && cudaMemsetAsync(status, 0, sizeof(int) * (size_t)E, st) != cudaSuccess) return HXG_ERR_CUDA;
     acoustics_geom_kernel<<<grid_for((long long)E * L * L * L, 256), 256, 0, st>>>(L, E, kind, params, tables,
                                                                                   F, status);
-    auto kern = acoustics_block_kernel<0>;
+    auto kern = acoustics_block_kernel<0, 0>;
+    const int dp = pr - p0;
     switch (p0) {
-    case 1: kern = acoustics_block_kernel<1>; break;
-    case 2: kern = acoustics_block_kernel<2>; break;
-    case 3: kern = acoustics_block_kernel<3>; break;
-    case 4: kern = acoustics_block_kernel<4>; break;
-    case 5: kern = acoustics_block_kernel<5>; break;
-    case 6: kern = acoustics_block_kernel<6>; break;
+#define HXG_AC_CASE(PP)                                                                   \
+    case PP:                                                                              \
+        kern = dp == 1 ? acoustics_block_kernel<PP, 1>                                    \
+                       : (dp == 2 ? acoustics_block_kernel<PP, 2> : acoustics_block_kernel<PP, 0>); \
+        break;
+        HXG_AC_CASE(1) HXG_AC_CASE(2) HXG_AC_CASE(3) HXG_AC_CASE(4)
+#undef HXG_AC_CASE
+    case 5: kern = acoustics_block_kernel<5, 0>; break;
+    case 6: kern = acoustics_block_kernel<6, 0>; break;
     default: break;
     }
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

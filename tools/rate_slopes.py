@@ -52,6 +52,8 @@ for (sp, path), v in sorted(pts.items()):
     s = {"space": sp, "path": path, "points": v}
     if len(hi) >= 3:
         s["slope_exec_dflop"] = slope([q["p_test"] for q in hi], [q["exec_dflop_per_element"] for q in hi])
-        s["slope_dram_write"] = slope([q["p_test"] for q in hi], [q["dram_write_bytes_per_element"] for q in hi])
+        # the operation counts are polynomials in L = p + 1 (digit extents p + 1, rule L):
+        # p^7 / p^6 of the paper are the leading powers, reached in L
+        s["slope_exec_dflop_vs_L"] = slope([q["p_test"] + 1 for q in hi], [q["exec_dflop_per_element"] for q in hi])
     out["series"].append(s)
 print(json.dumps(out, indent=1))
