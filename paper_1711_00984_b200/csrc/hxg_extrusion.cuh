@@ -67,7 +67,9 @@ struct ExtCfg {
 #ifdef HXG_EXT_C3
     static constexpr int C3 = HXG_EXT_C3;
 #else
-    static constexpr int C3 = (S == HDIV && P >= 6) ? 4 : 1;
+    // (H1 p = 7, n3 = 8: C3 = 2 measured 29 -> 49 % of the roofline; at every other H1 order
+    // C3 = 2 / 4 measured slower, 22-50 % vs 25-65 %)
+    static constexpr int C3 = (S == HDIV && P >= 6) ? 4 : ((S == H1 && P == 7) ? 2 : 1);
 #endif
     static constexpr bool VT = HXG_EXT_VT && C3 == 1;
     __host__ __device__ static constexpr int vt_slot(int L) { return VT ? 4 * KF * L : 0; }
