@@ -471,7 +471,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
     // stage-B B operand (Abar fragments) and this lane's trial-side 1D values are loaded
     // once per group
     constexpr bool AST = pw_astat(S);
-    constexpr bool HOIST = AST && C::K == 1 && HXG_PW_BHOIST;
+    constexpr bool HOIST = C::K == 1 && (HXG_PW_BHOIST > 1 || (AST && HXG_PW_BHOIST));
     constexpr int NRTA = AST ? NRT : 1;
     double areg[NRTA][NK];
     if constexpr (!AST) areg[0][0] = 0.0;
