@@ -35,10 +35,10 @@ namespace hxg {
 #endif
 constexpr int LO_THREADS = HXG_LO_THREADS;
 #ifndef HXG_LO_BUDGET_KB
-#define HXG_LO_BUDGET_KB 50  // shared memory per CTA (4 CTAs per SM: more barrier domains per SM measured +3-14 % over 2 x 256 threads)
+#define HXG_LO_BUDGET_KB 44  // shared memory per CTA (4 CTAs per SM: more barrier domains per SM measured +3-14 % over 2 x 256 threads)
 #endif
 #ifndef HXG_LO_MAXB
-#define HXG_LO_MAXB 4  // CTAs per SM (register budget 65536 / (MAXB * THREADS))
+#define HXG_LO_MAXB 5  // CTAs per SM (5 x 128 threads at <= 102 registers: +2-6 % over 4) (register budget 65536 / (MAXB * THREADS))
 #endif
 #ifndef HXG_LO_EBMAX
 #define HXG_LO_EBMAX 16  // most elements per CTA pass
