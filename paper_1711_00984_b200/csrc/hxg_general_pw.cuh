@@ -86,7 +86,7 @@ __host__ __device__ constexpr bool pw_direct(int S) { return HXG_PW_WO < 0 ? (S 
 #define HXG_PW_NSG_MAX 0  // > 0: short groups re-divide the staging area into up to this many slots (measured: no gain)
 #endif
 #ifndef HXG_PW_BHOIST
-#define HXG_PW_BHOIST 1  // A-stationary groups: stage-B B fragments and trial-side 1D values in registers
+#define HXG_PW_BHOIST 2  // stage-B B fragments (Abar) and trial-side 1D values in registers per group: 1 A-stationary groups only, 2 every group (direct spaces +0.2-3.5 % at p 8-10)
 #endif
 __host__ __device__ constexpr bool pw_astat(int S) { return HXG_PW_ASTAT < 0 ? !pw_direct(S) : HXG_PW_ASTAT == 1; }
 constexpr int PW_WARPS = HXG_PW_WARPS;
