@@ -88,6 +88,11 @@ __host__ __device__ constexpr bool pw_direct(int S) { return HXG_PW_WO < 0 ? (S 
 #ifndef HXG_PW_BHOIST
 #define HXG_PW_BHOIST 2  // stage-B B fragments (Abar) and trial-side 1D values in registers per group: 1 A-stationary groups only, 2 every group (direct spaces +0.2-3.5 % at p 8-10)
 #endif
+// direct spaces: block pairs whose group holds at most this many A-fragment doubles per lane
+// also keep them in registers (0: never; measured -2 to -4 % for H(curl) p 8-10 at 24 / 40)
+#ifndef HXG_PW_ASTAT_PAIR
+#define HXG_PW_ASTAT_PAIR 0
+#endif
 __host__ __device__ constexpr bool pw_astat(int S) { return HXG_PW_ASTAT < 0 ? !pw_direct(S) : HXG_PW_ASTAT == 1; }
 constexpr int PW_WARPS = HXG_PW_WARPS;
 constexpr int PW_THREADS = PW_WARPS * 32;
@@ -288,7 +293,7 @@ __device__ __forceinline__ void pw_bulk_prep(PWLane &ln, const double *sS, doubl
 
 // One stage-C step: CTW column tiles starting at column tile ct, all row tiles of the
 // group, then the staging stores of this lane's D fragments.
-template <int S, int P, int L, int A, int B, int NJ2, int NK, int CTW, int NRTA>
+template <int S, int P, int L, int A, int B, int NJ2, int NK, int CTW, bool ASTG, int NRTA>
 __device__ __forceinline__ void pw_step(const double *sT, const double *sB, double *sS, int ct, int seq,
                                         const int (&os)[NK], const int (&orr)[NK], PWLane &ln,
                                         const double (&areg)[NRTA][NK])
@@ -334,7 +339,7 @@ __device__ __forceinline__ void pw_step(const double *sT, const double *sB, doub
 #pragma unroll
         for (int rt = 0; rt < NRT; ++rt) {
             double a;
-            if constexpr (pw_astat(S)) a = areg[rt][ks];
+            if constexpr (ASTG) a = areg[rt][ks];  // A-stationary group
             else a = sB[(rt * NKS + ks) * 32 + lane];
 #pragma unroll
             for (int w = 0; w < CTW; ++w) dmma_8x8x4(d[w][rt][0], d[w][rt][1], a, Bp[w][ks]);
@@ -470,7 +475,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
     // A layout) into registers areg[rt][*], which stage C keeps for the whole group; the
     // stage-B B operand (Abar fragments) and this lane's trial-side 1D values are loaded
     // once per group
-    constexpr bool AST = pw_astat(S);
+    constexpr bool AST = pw_astat(S) || (C::K == 1 && NRT * NK <= HXG_PW_ASTAT_PAIR);
     constexpr bool HOIST = C::K == 1 && (HXG_PW_BHOIST > 1 || (AST && HXG_PW_BHOIST));
     constexpr int NRTA = AST ? NRT : 1;
     double areg[NRTA][NK];
@@ -563,7 +568,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
         int jnext;
         if constexpr (!pw_direct(S)) pw_bulk_prep<RJ * SEG, SEG, C12a>(ln, sS, outE, epar, I0, kc);
         if (st < NST) {
-            pw_step<S, P, L, A, B, NJ2, NK, CTW>(sT, sB, sS, ct, seq, os, orr, ln, areg);
+            pw_step<S, P, L, A, B, NJ2, NK, CTW, AST>(sT, sB, sS, ct, seq, os, orr, ln, areg);
             if constexpr (pw_direct(S)) {
                 jnext = ct + CTW < NCT ? ((ct + CTW) * 8) / n1a : n1b;
             } else {
@@ -572,7 +577,7 @@ __device__ __forceinline__ void pw_group(const double *sT, double *W, double *__
                 while (ln.ei1 >= n1a) { ln.ei1 -= n1a; ++ln.ej1; }
             }
         } else {
-            if constexpr (NCT % CTW != 0) pw_step<S, P, L, A, B, NJ2, NK, 1>(sT, sB, sS, ct, seq, os, orr, ln, areg);
+            if constexpr (NCT % CTW != 0) pw_step<S, P, L, A, B, NJ2, NK, 1, AST>(sT, sB, sS, ct, seq, os, orr, ln, areg);
             jnext = n1b;
         }
         // trial digits completed by this step: one bulk copy per segment (j1, jj2)
