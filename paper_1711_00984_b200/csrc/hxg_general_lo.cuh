@@ -40,6 +40,9 @@ constexpr int LO_THREADS = HXG_LO_THREADS;
 #ifndef HXG_LO_MAXB
 #define HXG_LO_MAXB 5  // CTAs per SM (5 x 128 threads at <= 102 registers: +2-6 % over 4) (register budget 65536 / (MAXB * THREADS))
 #endif
+#ifndef HXG_LO_J1U
+#define HXG_LO_J1U 1  // unroll factor of the stage-C trial-row loop (2 measured -4 to -18 %)
+#endif
 #ifndef HXG_LO_EBMAX
 #define HXG_LO_EBMAX 16  // most elements per CTA pass
 #endif
@@ -246,7 +249,8 @@ __device__ __forceinline__ void lo_item(const double *sT, const double *sU, cons
         // ---- stage C: D[j1][i1] = sum_{h,l} B_h[l] U_h[j1][i1][l] into the slab image
         const int Ib = offA + n1a * (i2 + n2a * i3);
         constexpr int UR = C::urow(A);
-#pragma unroll 1
+        constexpr int J1U = HXG_LO_J1U;
+#pragma unroll J1U
         for (int j1 = 0; j1 < n1b; ++j1) {
             const int J = offB + j1 + n1b * (j2 + n2b * j3);
             // image offset of (J, J): rows J0 .. J - 1 hold N - J' entries each
